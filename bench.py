@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""bench.py -- keys sorted/s of LearnedSort 2.0 on B200 (BASELINE.json metric).
+
+Default (N=1): BASELINE config 2's first distribution, 200M fp64 Normal(0,1)
+keys resident in HBM, sorted in place by ls_sort (sample + fit + two
+partition rounds + in-bucket sort, all timed). N>1 (torchrun): BASELINE config
+5, 1B fp64 keys per rank (50/50 Uniform[0,1e9) and Zipf(1.0) over 1e7 ranks,
+seed 1000+rank), global sort with ls_sort_multi (range split + NCCL all-to-all
++ local sort).
+
+Timing: W warm-up steps, then K timed steps between a barrier +
+cuda.synchronize on both sides; every step is timed with CUDA events on the
+launching stream around the sort call only (the pristine input is restored by
+an untimed device copy before each step; the 1.6 GB input is larger than the
+126 MB L2, so no flush is needed). Max over ranks. Prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, single-threaded) as the
+reference arm on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "keys sorted/sec (fp64/uint64) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "keys/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def phase_bytes(phase: str, n: int, st: dict) -> float:
+    """Algorithmic HBM bytes of one launch of a phase, 8-byte keys."""
+    h0 = st["h0_keys"]
+    if phase == "count0":
+        return 8.0 * n
+    if phase == "scatter0":
+        return 16.0 * n
+    if phase == "count1":
+        return 8.0 * n
+    if phase == "scatter1":
+        return 16.0 * (n - h0) + 8.0 * h0
+    if phase == "bucketsort":
+        return 16.0 * st["small_keys"] + 8.0 * (st["h1_keys"])
+    if phase == "big":
+        return 40.0 * st["big_keys"]
+    if phase == "fit":
+        return 32.0 * (n / 100.0)
+    return 0.0
+
+
+def design_bytes(n: int, st: dict) -> float:
+    return sum(phase_bytes(p, n, st) for p in ("fit", "count0", "scatter0", "count1", "scatter1",
+                                                "bucketsort", "big"))
+
+
+def traffic_from_profiles(phase: str, n: int):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    e = d.get(phase)
+    if not e or e.get("n") != n:
+        return None
+    return e.get("dram_bytes_per_launch")
+
+
+# ----------------------------------------------------------------- ours ----
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_2107_03290_b200 as ls
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+
+    multi = world > 1
+    wl = args.workload or ("c5_mix" if multi else "c2_normal")
+    dist_name, seed = datagen.WORKLOADS[wl]
+    if wl == "c5_mix":
+        seed = 1000 + rank
+    n = args.n or (1_000_000_000 if multi else 200_000_000)
+    plan = datagen.Plan(dist_name, n, seed)
+    tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
+    pristine = torch.empty(n, dtype=tdt, device=dev)
+    plan.device(pristine)
+    keys = torch.empty_like(pristine)
+    cfg = ls.config(flags=ls.LS_FLAG_PHASE_TIMING)
+    dt = ls.dtype_code(pristine)
+    if multi:
+        comm = ls.Comm.from_torch_distributed()
+        out_cap = int(n * 1.25) + 1_000_000
+        out = torch.empty(out_cap, dtype=tdt, device=dev)
+        ws = torch.empty(ls.multi_workspace_bytes(n, out_cap, world, dt, cfg), dtype=torch.uint8,
+                         device=dev)
+    else:
+        ws = ls.workspace(n, dt, cfg, dev)
+    torch.cuda.synchronize()
+
+    def one_step():
+        keys.copy_(pristine)  # untimed restore
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_out = n
+        if multi:
+            n_out, st = ls.ls_sort_multi(comm, keys, out, cfg=cfg, ws=ws, stream=stream)
+        else:
+            st = ls.ls_sort(keys, cfg=cfg, ws=ws, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), st, n_out
+
+    for _ in range(args.warmup):
+        one_step()
+    if multi:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, stats = [], []
+    with ClockSampler(local) as clk:
+        if multi:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            ms, st, n_out = one_step()
+            times.append(ms)
+            stats.append(st)
+        torch.cuda.synchronize()
+        if multi:
+            dist.barrier()
+    total_ms = sum(times)
+    if multi:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    keys_total = n * world * args.steps
+    value = keys_total / (total_ms / 1e3)
+
+    # per-phase device times (CUDA events recorded by libls on `stream`)
+    st0 = stats[-1]
+    phase_ms = {p: statistics.mean(s["phase_ms"][p] for s in stats) for p in ls.PHASES}
+    n_local = st0["n"]
+    dom = max((p for p in ls.PHASES if p != "fit"), key=lambda p: phase_ms[p])
+    peak, peak_src = load_peaks()
+    b = phase_bytes(dom, n_local, st0)
+    achieved = b / (phase_ms[dom] / 1e3) / 1e9
+    step_ms = total_ms / args.steps
+    dbytes = design_bytes(n_local, st0)
+
+    # correctness guard on the last step (cheap, on device): output non-decreasing
+    res = (out[: n_out] if multi else keys)
+    u = res.view(torch.int64)
+    if res.dtype == torch.float64:
+        o = torch.where(u < 0, ~u, u ^ torch.iinfo(torch.int64).min)
+    else:
+        o = u ^ torch.iinfo(torch.int64).min
+    sorted_ok = bool((o[1:] >= o[:-1]).all().item())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dt == ls.LS_F64 else "u64",
+        "data": "synthetic (device Philox4x32-10 generator, datagen/)",
+        "config": {"workload": wl, "distribution": dist_name, "seed": seed, "n_per_gpu": n,
+                   "n_total": n * world, "l2": "inputs (8n bytes) larger than the 126 MB L2; "
+                   "pristine input restored by an untimed D2D copy before each step",
+                   "timed": "ls_sort_multi (split + all-to-all + local sort)" if multi else
+                   "ls_sort: sample + fit + count0 + scatter0 + count1 + scatter1 + classify + "
+                   "bucketsort + big path", "parallelism": f"range split x{world}" if multi else "1 GPU"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profiles(dom, n_local),
+                     "algorithmic_bytes_per_launch": b, "avg_launch_ms": phase_ms[dom],
+                     "peak_source": peak_src},
+        "hbm_roofline_step": {"design_bytes": dbytes, "bytes_per_key": dbytes / n_local,
+                              "achieved_gbs": dbytes / (step_ms / 1e3) / 1e9,
+                              "frac": dbytes / (step_ms / 1e3) / 1e9 / peak,
+                              "frac_8tbs": dbytes / (step_ms / 1e3) / 1e9 / 8000.0},
+        "phase_ms": phase_ms,
+        "class_keys": {k: st0[k] for k in ("h0_keys", "h1_keys", "small_keys", "big_keys",
+                                           "big_subbuckets", "max_group")},
+        "sorted_ok": sorted_ok,
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "clocks": clk.summary(),
+    }
+    if multi:
+        line["n_out_rank0"] = n_out
+
+    # e2e: same metric through the C ABI with HOST buffers (ls_sort_host), copies timed
+    if not multi and not args.no_e2e:
+        host = torch.empty(n, dtype=tdt, pin_memory=True)
+        host_pristine = pristine.cpu()
+        e2e_ms = []
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            host.copy_(host_pristine)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ls.ls_sort_host(host, keys, cfg=cfg, ws=ws, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            if i > 0:
+                e2e_ms.append(e0.elapsed_time(e1))
+        line["e2e"] = {"value": n / (statistics.mean(e2e_ms) / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                       "ms_per_step": statistics.mean(e2e_ms), "api": "ls_sort_host"}
+
+    # CPU baseline: the oracle as it stands, rank 0 at N=1, bounded sample
+    if not multi and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(plan, args.cpu_sample)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if multi:
+        comm.close()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(plan, count: int) -> dict:
+    import oracle
+    count = min(count, plan.n)
+    h = plan_host_prefix(plan, count)
+    t0 = time.perf_counter()
+    oracle.sort(h)
+    dt = time.perf_counter() - t0
+    return {"value": count / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {count} keys of the {plan.dist} workload (same device-generated "
+                      f"bytes), oracle/ls2_oracle.c single-threaded, {dt:.1f} s",
+            "host_cpu": host_cpu()}
+
+
+def plan_host_prefix(plan, count):
+    """Device-generate the first `count` keys and copy them to the host."""
+    import numpy as np
+    import torch
+    tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
+    t = torch.empty(count, dtype=tdt, device="cuda")
+    plan.device(t)
+    torch.cuda.synchronize()
+    a = t.view(torch.int64).cpu().numpy().view(np.uint64)
+    return a.view(np.float64) if plan.dtype == np.float64 else a
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical cores)"
+    except OSError:
+        pass
+    return None
+
+
+# ------------------------------------------------------------ reference ----
+
+def run_reference(args):
+    """The base contract's reference arm is, for this tier, the oracle."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import datagen
+    import oracle
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    wl = args.workload or ("c5_mix" if world > 1 else "c2_normal")
+    dist_name, seed = datagen.WORKLOADS[wl]
+    if wl == "c5_mix":
+        seed = 1000
+    n = args.n or (1_000_000_000 if world > 1 else 200_000_000)
+    count = min(args.ref_sample, n)
+    plan = datagen.Plan(dist_name, n, seed)
+    try:
+        import torch
+        have_gpu = torch.cuda.is_available()
+    except Exception:
+        have_gpu = False
+    h = plan_host_prefix(plan, count) if have_gpu else plan.host(0, count)
+    for _ in range(args.warmup):
+        oracle.sort(h)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sort(h)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = count * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if plan.dtype == np.float64 else "u64", "data": "synthetic",
+        "config": {"workload": wl, "distribution": dist_name, "seed": seed, "n_per_gpu": n,
+                   "sample_per_step": count},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {count} keys of the {wl} workload per step",
+                         "host_cpu": host_cpu()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default=None, help="a key of datagen.WORKLOADS")
+    ap.add_argument("--n", type=int, default=0, help="keys per GPU (default: the config's)")
+    ap.add_argument("--cpu-sample", type=int, default=100_000_000)
+    ap.add_argument("--ref-sample", type=int, default=10_000_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup < 3 is below the contract minimum", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,505 @@
+// ls_api.cu -- C ABI of libls (include/ls.h): workspace layout, the launch
+// sequence of Alg. 2 on one GPU, status/stats, and the parity hooks.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <memory>
+#include <string>
+
+#include "ls.h"
+#include "ls_api_internal.h"
+#include "ls_launch.h"
+
+namespace ls {
+
+static thread_local std::string g_err;
+
+void set_error(const char *msg) { g_err = msg ? msg : ""; }
+
+static ls_status cuda_fail(const char *where, cudaError_t e) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    set_error(buf);
+    return LS_E_CUDA;
+}
+
+#define LS_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(#call, e_); \
+    } while (0)
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Workspace layout. Three groups, each contiguous: arrays set to 0xFF, arrays
+// set to 0, arrays written before being read.
+struct Layout {
+    uint64_t n, m;
+    int f, L;
+    uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
+    size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
+        lb1, offs1, hist1, start1, tfirst, tlast, big, hist1_u64, B;
+    size_t ff_begin, ff_end, zero_begin, zero_end, total;
+};
+
+static Layout make_layout(uint64_t n, const ls_config &cfg) {
+    Layout l;
+    memset(&l, 0, sizeof l);
+    l.n = n;
+    l.f = (int)cfg.fanout;
+    l.L = (int)cfg.leaf_count;
+    l.m = (n + cfg.sample_stride - 1) / cfg.sample_stride;
+    l.C0 = 65536;
+    l.C1 = 65536;
+    l.U0 = (uint32_t)((n + l.C0 - 1) / l.C0);
+    if (l.U0 == 0) l.U0 = 1;
+    l.U1max = (uint32_t)((n + l.C1 - 1) / l.C1) + (uint32_t)l.f;
+    l.T_small = cfg.big_threshold;
+    l.T_tile = cfg.big_threshold;
+    l.ntiles = (uint32_t)((n + l.T_tile - 1) / l.T_tile);
+    if (l.ntiles == 0) l.ntiles = 1;
+    const uint64_t ff = (uint64_t)l.f * l.f;
+    l.big_cap = (uint32_t)((n / (l.T_small + 1) + 1) < ff ? (n / (l.T_small + 1) + 1) : ff);
+    if (l.big_cap < 64) l.big_cap = 64;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = align_up(off, 256);
+        off = o + bytes;
+        return o;
+    };
+    l.ff_begin = align_up(off, 256);
+    l.leaf_min = take((size_t)l.L * 8);
+    l.bmin0 = take((size_t)l.f * 8);
+    l.tfirst = take((size_t)l.ntiles * 4);
+    l.ff_end = off;
+    l.zero_begin = align_up(off, 256);
+    l.leaf_cnt = take((size_t)l.L * 4);
+    l.hist0 = take((size_t)l.f * 8);
+    l.bmax0 = take((size_t)l.f * 8);
+    l.lb0 = take((size_t)l.U0 * l.f * 8);
+    l.lb1 = take((size_t)l.U1max * l.f * 8);
+    l.hist1 = take(ff * 4);
+    l.tlast = take((size_t)l.ntiles * 4);
+    l.zero_end = off;
+    l.ctl = take(sizeof(Ctl));
+    l.model = take(sizeof(DevModel));
+    l.S = take((size_t)l.m * 8);
+    l.start0 = take((size_t)(l.f + 1) * 8);
+    l.ustart = take((size_t)(l.f + 1) * 4);
+    l.offs0 = take((size_t)l.U0 * l.f * 4);
+    l.offs1 = take((size_t)l.U1max * l.f * 4);
+    l.start1 = take(ff * 4);
+    l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
+    l.hist1_u64 = take(ff * 8);
+    l.B = take((size_t)n * 8);
+    l.total = align_up(off, 256);
+    return l;
+}
+
+static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
+    unsigned char *w = (unsigned char *)d_ws;
+    Args a;
+    memset(&a, 0, sizeof a);
+    a.A = (uint64_t *)d_keys;
+    a.B = (uint64_t *)(w + l.B);
+    a.n = l.n;
+    a.f = l.f;
+    a.L = l.L;
+    a.F = (double)l.f;
+    a.F2 = (double)l.f * (double)l.f;
+    a.nd = (double)l.n;
+    a.C0 = l.C0;
+    a.C1 = l.C1;
+    a.U0 = l.U0;
+    a.U1max = l.U1max;
+    a.T_small = l.T_small;
+    a.T_tile = l.T_tile;
+    a.ntiles = l.ntiles;
+    a.big_cap = l.big_cap;
+    a.ctl = (Ctl *)(w + l.ctl);
+    a.M = (DevModel *)(w + l.model);
+    a.S = (uint64_t *)(w + l.S);
+    a.leaf_cnt = (uint32_t *)(w + l.leaf_cnt);
+    a.leaf_min = (unsigned long long *)(w + l.leaf_min);
+    a.hist0 = (unsigned long long *)(w + l.hist0);
+    a.start0 = (unsigned long long *)(w + l.start0);
+    a.bmin0 = (unsigned long long *)(w + l.bmin0);
+    a.bmax0 = (unsigned long long *)(w + l.bmax0);
+    a.unit1_start = (uint32_t *)(w + l.ustart);
+    a.lb0 = (unsigned long long *)(w + l.lb0);
+    a.offs0 = (uint32_t *)(w + l.offs0);
+    a.lb1 = (unsigned long long *)(w + l.lb1);
+    a.offs1 = (uint32_t *)(w + l.offs1);
+    a.hist1 = (uint32_t *)(w + l.hist1);
+    a.start1 = (uint32_t *)(w + l.start1);
+    a.tile_first = (uint32_t *)(w + l.tfirst);
+    a.tile_last = (uint32_t *)(w + l.tlast);
+    a.big = (BigItem *)(w + l.big);
+    return a;
+}
+
+static ls_status check_config(const ls_config &c) {
+    if (c.fanout < 2 || c.fanout > LS_MAX_FANOUT) { set_error("fanout out of range [2, 1024]"); return LS_E_INVALID; }
+    if (c.leaf_count < 1 || c.leaf_count > LS_MAX_LEAVES) { set_error("leaf_count out of range [1, 1024]"); return LS_E_INVALID; }
+    if (c.sample_stride < 1) { set_error("sample_stride must be >= 1"); return LS_E_INVALID; }
+    if (c.fit != 0) { set_error("only the chord fit (0) is implemented"); return LS_E_INVALID; }
+    if (c.big_threshold < 64 || c.big_threshold > 4096) { set_error("big_threshold out of range [64, 4096]"); return LS_E_INVALID; }
+    return LS_OK;
+}
+
+static void to_dev_model(const ls_model &h, DevModel &d) {
+    memset(&d, 0, sizeof d);
+    d.xmin = h.xmin;
+    d.xmax = h.xmax;
+    d.root_scale = h.root_scale;
+    d.L = h.leaf_count;
+    d.last = (double)(h.leaf_count - 1);
+    d.degenerate = h.degenerate;
+    d.n_sample = h.n_sample;
+    for (uint32_t l = 0; l < h.leaf_count; l++) {
+        d.leaf[5 * l + 0] = h.leaf[l].a;
+        d.leaf[5 * l + 1] = h.leaf[l].c;
+        d.leaf[5 * l + 2] = h.leaf[l].b;
+        d.leaf[5 * l + 3] = h.leaf[l].lo;
+        d.leaf[5 * l + 4] = h.leaf[l].hi;
+    }
+}
+
+static void from_dev_model(const DevModel &d, int dtype, ls_model &h) {
+    memset(&h, 0, sizeof h);
+    h.dtype = (uint32_t)dtype;
+    h.leaf_count = d.L;
+    h.n_sample = d.n_sample;
+    h.degenerate = d.degenerate;
+    h.xmin = d.xmin;
+    h.xmax = d.xmax;
+    h.root_scale = d.root_scale;
+    for (uint32_t l = 0; l < d.L && l < LS_MAX_LEAVES; l++) {
+        h.leaf[l].a = d.leaf[5 * l + 0];
+        h.leaf[l].c = d.leaf[5 * l + 1];
+        h.leaf[l].b = d.leaf[5 * l + 2];
+        h.leaf[l].lo = d.leaf[5 * l + 3];
+        h.leaf[l].hi = d.leaf[5 * l + 4];
+    }
+}
+
+// The model is monotone-safe (so the touch-up only needs collision groups, R15)
+static bool model_ok(const ls_model &m, const ls_config &cfg) {
+    const double PM = 1.0 - 0x1p-52;
+    if (m.leaf_count < 1 || m.leaf_count > LS_MAX_LEAVES) return false;
+    if (!(m.xmin <= m.xmax) || !(m.root_scale >= 0.0)) return false;
+    if (!isfinite(m.xmin) || !isfinite(m.xmax) || !isfinite(m.root_scale)) return false;
+    for (uint32_t l = 0; l < m.leaf_count; l++) {
+        const ls_leaf &q = m.leaf[l];
+        if (!isfinite(q.a) || !isfinite(q.b) || !isfinite(q.c) || !isfinite(q.lo) || !isfinite(q.hi)) return false;
+        if (!(q.a >= 0.0) || !(q.lo >= 0.0) || !(q.lo <= q.hi) || !(q.hi <= PM)) return false;
+        if (l + 1 < m.leaf_count && !(q.hi <= m.leaf[l + 1].lo)) return false;
+    }
+    (void)cfg;
+    return true;
+}
+
+struct Timer {
+    bool on = false;
+    cudaEvent_t ev[LS_NUM_PHASES + 1];
+    int phase_of[LS_NUM_PHASES + 1];
+    int k = 0;
+    cudaStream_t st;
+    void start(bool enable, cudaStream_t s) {
+        on = enable;
+        st = s;
+        if (!on) return;
+        for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventCreate(&ev[i]);
+        cudaEventRecord(ev[0], st);
+        k = 0;
+    }
+    void mark(int phase) {
+        if (!on) return;
+        phase_of[k] = phase;
+        cudaEventRecord(ev[++k], st);
+    }
+    void finish(ls_stats *s) {
+        if (!on) return;
+        if (s)
+            for (int i = 0; i < k; i++) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+                s->phase_ms[phase_of[i]] += ms;
+            }
+        for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(ev[i]);
+        on = false;
+    }
+};
+
+// Enqueue the whole sort. If `sync` the stream is synchronised and the status
+// and stats are collected; otherwise the caller synchronises (ls_sort_host).
+ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg_in,
+                       const ls_model *inject, void *d_ws, size_t ws_bytes, cudaStream_t st,
+                       ls_stats *stats, const ls_dumps *dumps, Pending *pend) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    ls_status rc = check_config(cfg);
+    if (rc != LS_OK) return rc;
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    if (n >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    if (stats) memset(stats, 0, sizeof *stats);
+    if (stats) stats->n = n;
+    if (n <= 1) return LS_OK;
+    if (!d_keys || !d_ws) { set_error("null pointer"); return LS_E_INVALID; }
+    if (inject && !model_ok(*inject, cfg)) { set_error("injected model is not monotone-safe"); return LS_E_INVALID; }
+    const Layout l = make_layout(n, cfg);
+    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    Args a = make_args(l, d_keys, d_ws);
+    const int dt = (int)dtype;
+    unsigned char *w = (unsigned char *)d_ws;
+    if (dumps) {
+        a.dH0 = dumps->d_H0;
+        a.dH1 = dumps->d_H1;
+        if (a.dH0) LS_CUDA(cudaMemsetAsync(a.dH0, 0, (size_t)l.f, st));
+        if (a.dH1) LS_CUDA(cudaMemsetAsync(a.dH1, 0, (size_t)l.f * l.f, st));
+    }
+    Timer tm;
+    tm.start(cfg.flags & LS_FLAG_PHASE_TIMING, st);
+    uint64_t launches = 0;
+    LS_CUDA(cudaMemsetAsync(w + l.ff_begin, 0xff, l.ff_end - l.ff_begin, st));
+    LS_CUDA(cudaMemsetAsync(w + l.zero_begin, 0, l.zero_end - l.zero_begin, st));
+    launch_init(a, st);
+    launches++;
+    if (inject) {
+        std::unique_ptr<DevModel> dm(new DevModel);
+        to_dev_model(*inject, *dm);
+        LS_CUDA(cudaMemcpyAsync(a.M, dm.get(), sizeof(DevModel), cudaMemcpyHostToDevice, st));
+        LS_CUDA(cudaStreamSynchronize(st));  // the staging buffer dies here
+    } else {
+        // north_star (1): strided sample (R9) + chord fit (R7)
+        launch_sample_minmax(a.A, cfg.sample_stride, l.m, a.S, a.ctl, dt, st);
+        launch_fit_hist(a.S, l.m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, dt, st);
+        launch_fit_params(l.m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, a.M, dt, st);
+        launches += 3;
+    }
+    tm.mark(LS_PHASE_FIT);
+    launch_count0(a, dt, st);
+    launch_plan0(a, dumps ? dumps->d_S_B : nullptr, st);
+    launches += 2;
+    tm.mark(LS_PHASE_COUNT0);
+    launch_scatter0(a, dt, st);
+    launches++;
+    tm.mark(LS_PHASE_SCATTER0);
+    launch_count1(a, dt, st);
+    launches++;
+    tm.mark(LS_PHASE_COUNT1);
+    launch_scatter1(a, dt, st);
+    launches++;
+    tm.mark(LS_PHASE_SCATTER1);
+    launch_classify(a, nullptr, st);
+    launches++;
+    if (dumps && dumps->d_S_B1)
+        LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
+    tm.mark(LS_PHASE_CLASSIFY);
+    launch_bucketsort(a, dt, st);
+    launches++;
+    tm.mark(LS_PHASE_BUCKETSORT);
+    for (int lv = 0; lv < BIG_LEVELS; lv++) {
+        launch_big(a, lv, dt, st);
+        launches++;
+    }
+    tm.mark(LS_PHASE_BIG);
+    LS_CUDA(cudaGetLastError());
+    pend->ctl_dev = a.ctl;
+    pend->model_dev = a.M;
+    pend->launches = launches;
+    pend->dtype = dt;
+    pend->timer_on = tm.on;
+    if (tm.on) {
+        memcpy(pend->ev, tm.ev, sizeof tm.ev);
+        memcpy(pend->phase_of, tm.phase_of, sizeof tm.phase_of);
+        pend->nmarks = tm.k;
+    }
+    LS_CUDA(cudaMemcpyAsync(&pend->ctl_host, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    if (dumps && dumps->h_model) {
+        pend->model_host.reset(new DevModel);
+        LS_CUDA(cudaMemcpyAsync(pend->model_host.get(), a.M, sizeof(DevModel), cudaMemcpyDeviceToHost, st));
+        pend->model_out = dumps->h_model;
+    }
+    pend->active = true;
+    return LS_OK;
+}
+
+ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
+    if (!pend->active) return LS_OK;
+    pend->active = false;
+    LS_CUDA(cudaStreamSynchronize(st));
+    const Ctl &c = pend->ctl_host;
+    if (stats) {
+        stats->h0_buckets = c.stat[ST_H0B];
+        stats->h0_keys = c.stat[ST_H0K];
+        stats->h1_subbuckets = c.stat[ST_H1S];
+        stats->h1_keys = c.stat[ST_H1K];
+        stats->small_subbuckets = c.stat[ST_SMALLS];
+        stats->small_keys = c.stat[ST_SMALLK];
+        stats->big_subbuckets = c.stat[ST_BIGS];
+        stats->big_keys = c.stat[ST_BIGK];
+        stats->max_group = c.stat[ST_MAXGRP];
+        stats->big_passes = c.stat[ST_BIGPASS];
+        stats->kernel_launches = pend->launches;
+    }
+    if (pend->timer_on) {
+        if (stats)
+            for (int i = 0; i < pend->nmarks; i++) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, pend->ev[i], pend->ev[i + 1]);
+                stats->phase_ms[pend->phase_of[i]] += ms;
+            }
+        for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(pend->ev[i]);
+    }
+    if (pend->model_out && pend->model_host) from_dev_model(*pend->model_host, pend->dtype, *pend->model_out);
+    if (c.status & STATUS_NAN) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
+    if (c.status & STATUS_INTERNAL) { set_error("internal invariant violated (corrupt partition state)"); return LS_E_INTERNAL; }
+    return LS_OK;
+}
+
+size_t workspace_bytes(uint64_t n, const ls_config &cfg) { return make_layout(n, cfg).total; }
+
+}  // namespace ls
+
+using namespace ls;
+
+extern "C" {
+
+void ls_config_default(ls_config *c) {
+    memset(c, 0, sizeof *c);
+    c->fanout = 1000;
+    c->leaf_count = 1000;
+    c->sample_stride = 100; // P:328 1% sample (R9)
+    c->fit = 0;
+    c->big_threshold = 2048;
+    c->flags = 0;
+}
+
+const char *ls_status_string(ls_status s) {
+    switch (s) {
+    case LS_OK: return "LS_OK";
+    case LS_E_INVALID: return "LS_E_INVALID";
+    case LS_E_NAN: return "LS_E_NAN";
+    case LS_E_WORKSPACE: return "LS_E_WORKSPACE";
+    case LS_E_CAPACITY: return "LS_E_CAPACITY";
+    case LS_E_CUDA: return "LS_E_CUDA";
+    case LS_E_NCCL: return "LS_E_NCCL";
+    case LS_E_INTERNAL: return "LS_E_INTERNAL";
+    }
+    return "LS_E_UNKNOWN";
+}
+
+const char *ls_last_error(void) { return g_err.c_str(); }
+
+ls_status ls_workspace_bytes(uint64_t n, ls_dtype dtype, const ls_config *cfg_in, size_t *bytes) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    ls_status rc = check_config(cfg);
+    if (rc != LS_OK) return rc;
+    if (dtype != LS_F64 && dtype != LS_U64) return LS_E_INVALID;
+    if (!bytes) return LS_E_INVALID;
+    *bytes = workspace_bytes(n, cfg);
+    return LS_OK;
+}
+
+ls_status ls_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg, void *d_ws,
+                  size_t ws_bytes, void *stream, ls_stats *stats, const ls_dumps *dumps) {
+    Pending p;
+    cudaStream_t st = (cudaStream_t)stream;
+    ls_status rc = enqueue_sort(d_keys, n, dtype, cfg, nullptr, d_ws, ws_bytes, st, stats, dumps, &p);
+    if (rc != LS_OK) return rc;
+    return finish_sort(&p, st, stats);
+}
+
+ls_status ls_sort_with_model(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg,
+                             const ls_model *model, void *d_ws, size_t ws_bytes, void *stream,
+                             ls_stats *stats, const ls_dumps *dumps) {
+    if (!model) { set_error("null model"); return LS_E_INVALID; }
+    Pending p;
+    cudaStream_t st = (cudaStream_t)stream;
+    ls_status rc = enqueue_sort(d_keys, n, dtype, cfg, model, d_ws, ws_bytes, st, stats, dumps, &p);
+    if (rc != LS_OK) return rc;
+    return finish_sort(&p, st, stats);
+}
+
+ls_status ls_sort_host(void *h_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg, void *d_buf,
+                       void *d_ws, size_t ws_bytes, void *stream, ls_stats *stats) {
+    if (n == 0) return LS_OK;
+    if (!h_keys || !d_buf) { set_error("null pointer"); return LS_E_INVALID; }
+    cudaStream_t st = (cudaStream_t)stream;
+    LS_CUDA(cudaMemcpyAsync(d_buf, h_keys, n * 8, cudaMemcpyHostToDevice, st));
+    Pending p;
+    ls_status rc = enqueue_sort(d_buf, n, dtype, cfg, nullptr, d_ws, ws_bytes, st, stats, nullptr, &p);
+    if (rc != LS_OK) return rc;
+    LS_CUDA(cudaMemcpyAsync(h_keys, d_buf, n * 8, cudaMemcpyDeviceToHost, st));
+    return finish_sort(&p, st, stats);
+}
+
+ls_status ls_train_rmi(const void *d_sample, uint64_t m, ls_dtype dtype, const ls_config *cfg_in,
+                       ls_model *out, void *d_ws, size_t ws_bytes, void *stream) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    ls_status rc = check_config(cfg);
+    if (rc != LS_OK) return rc;
+    if (!out || !d_ws || (m && !d_sample)) { set_error("null pointer"); return LS_E_INVALID; }
+    if (m == 0) { set_error("empty sample (S:59)"); return LS_E_INVALID; }
+    if (dtype != LS_F64 && dtype != LS_U64) return LS_E_INVALID;
+    cfg.sample_stride = 1;
+    const Layout l = make_layout(m, cfg);
+    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    Args a = make_args(l, nullptr, d_ws);
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned char *w = (unsigned char *)d_ws;
+    LS_CUDA(cudaMemsetAsync(w + l.ff_begin, 0xff, l.ff_end - l.ff_begin, st));
+    LS_CUDA(cudaMemsetAsync(w + l.zero_begin, 0, l.zero_end - l.zero_begin, st));
+    launch_init(a, st);
+    const uint64_t *S = (const uint64_t *)d_sample;
+    launch_sample_minmax(S, 1, m, nullptr, a.ctl, (int)dtype, st);
+    launch_fit_hist(S, m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, (int)dtype, st);
+    launch_fit_params(m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, a.M, (int)dtype, st);
+    LS_CUDA(cudaGetLastError());
+    std::unique_ptr<DevModel> dm(new DevModel);
+    LS_CUDA(cudaMemcpyAsync(dm.get(), a.M, sizeof(DevModel), cudaMemcpyDeviceToHost, st));
+    LS_CUDA(cudaStreamSynchronize(st));
+    from_dev_model(*dm, (int)dtype, *out);
+    return LS_OK;
+}
+
+ls_status ls_bucket_ids(const void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg_in,
+                        const ls_model *model, double *d_p, uint32_t *d_b0, uint32_t *d_b1,
+                        uint32_t *d_pos, uint64_t *d_hist0, uint64_t *d_hist1, void *d_ws,
+                        size_t ws_bytes, void *stream) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    ls_status rc = check_config(cfg);
+    if (rc != LS_OK) return rc;
+    if (!model || !d_ws) { set_error("null pointer"); return LS_E_INVALID; }
+    if (!model_ok(*model, cfg)) { set_error("model is not monotone-safe"); return LS_E_INVALID; }
+    if (dtype != LS_F64 && dtype != LS_U64) return LS_E_INVALID;
+    const Layout l = make_layout(n, cfg);
+    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    unsigned char *w = (unsigned char *)d_ws;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevModel *M = (DevModel *)(w + l.model);
+    std::unique_ptr<DevModel> dm(new DevModel);
+    to_dev_model(*model, *dm);
+    LS_CUDA(cudaMemcpyAsync(M, dm.get(), sizeof(DevModel), cudaMemcpyHostToDevice, st));
+    const size_t ff = (size_t)l.f * l.f;
+    unsigned long long *h1 = d_hist1 ? (unsigned long long *)d_hist1 : (unsigned long long *)(w + l.hist1_u64);
+    unsigned long long *h0 = (unsigned long long *)d_hist0;
+    if (h0) LS_CUDA(cudaMemsetAsync(h0, 0, (size_t)l.f * 8, st));
+    const bool need_h1 = d_hist1 || d_pos;
+    if (need_h1) LS_CUDA(cudaMemsetAsync(h1, 0, ff * 8, st));
+    if (n) {
+        launch_bucket_ids((const uint64_t *)d_keys, n, l.f, M, d_p, d_b0, d_b1, h0,
+                          need_h1 ? h1 : nullptr, (int)dtype, st);
+        if (d_pos) launch_bucket_pos((const uint64_t *)d_keys, n, l.f, M, h1, d_pos, (int)dtype, st);
+    }
+    LS_CUDA(cudaGetLastError());
+    LS_CUDA(cudaStreamSynchronize(st));
+    return LS_OK;
+}
+
+}  // extern "C"

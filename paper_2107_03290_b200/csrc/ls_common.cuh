@@ -1,0 +1,242 @@
+// ls_common.cuh -- device-side building blocks of libls (sm_100a).
+//
+// The fp64 arithmetic here is the bit-exact contract with the oracle's readings
+// R7-R13: explicit round-to-nearest intrinsics so that nvcc never
+// contracts a multiply-add except the leaf line's single fma (R13).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ls.h"
+
+namespace ls {
+
+enum { DT_F64 = 0, DT_U64 = 1 };
+
+constexpr double PMAX = 1.0 - 0x1p-52;  // R10
+constexpr uint64_t LB_FLAG_A = 1ull << 62;  // decoupled lookback: aggregate published
+constexpr uint64_t LB_FLAG_P = 2ull << 62;  // decoupled lookback: inclusive prefix published
+constexpr uint64_t LB_VALUE = (1ull << 62) - 1;
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// --------------------------------------------------------------- keys ------
+template <int DT>
+__device__ __forceinline__ uint64_t to_ord(uint64_t b) {
+    if (DT == DT_U64) return b;
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+template <int DT>
+__device__ __forceinline__ uint64_t from_ord(uint64_t o) {
+    if (DT == DT_U64) return o;
+    return (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+}
+template <int DT>
+__device__ __forceinline__ double xd(uint64_t b) {
+    if (DT == DT_U64) return __ull2double_rn(b);
+    return __longlong_as_double((long long)b);
+}
+template <int DT>
+__device__ __forceinline__ bool is_finite_key(uint64_t b) {
+    if (DT == DT_U64) return true;
+    return (b & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+}
+__device__ __forceinline__ bool is_nan_bits(uint64_t b) {
+    return (b & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
+}
+// R13: ordered comparisons, NaN -> lo, never fmin/fmax
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+    return v >= lo ? (v <= hi ? v : hi) : lo;
+}
+
+// -------------------------------------------------------------- model ------
+// Device copy of F_A. leaf[] holds (a, c, b, lo, hi) per leaf, 40 bytes.
+struct DevModel {
+    double xmin, xmax, root_scale, last;  // last = (double)(L-1)
+    uint32_t L, degenerate;
+    uint64_t n_sample;
+    double leaf[LS_MAX_LEAVES * 5];
+};
+
+// Root parameters held in registers (uniform across the grid).
+struct Root {
+    double xmin, xmax, rs, last;
+    int Lm1;
+};
+
+__device__ __forceinline__ Root load_root(const DevModel *M) {
+    Root r;
+    r.xmin = M->xmin;
+    r.xmax = M->xmax;
+    r.rs = M->root_scale;
+    r.last = M->last;
+    r.Lm1 = (int)M->L - 1;
+    return r;
+}
+
+// O6: p = F_A(x). `leaf` may point to shared or global memory.
+template <int DT>
+__device__ __forceinline__ double predict(uint64_t bits, const Root &R, const double *leaf) {
+    double xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
+    double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    int l = (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+    const double *q = leaf + 5 * l;
+    double y = __fma_rn(q[0], __dsub_rn(xc, q[1]), q[2]);
+    return __dadd_rn(clampd(y, q[3], q[4]), 0.0);
+}
+
+// Same, reading leaf parameters through the read-only path (keys of one
+// level-0 bucket share one or two leaves, so a warp's loads mostly broadcast).
+template <int DT>
+__device__ __forceinline__ double predict_ldg(uint64_t bits, const Root &R, const double *leaf) {
+    double xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
+    double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    int l = (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+    const double *q = leaf + 5 * l;
+    double y = __fma_rn(__ldg(q), __dsub_rn(xc, __ldg(q + 1)), __ldg(q + 2));
+    return __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
+}
+
+// O7 / Alg.1 P:107 (R1)
+__device__ __forceinline__ uint32_t bucket0(double p, double F, int f) {
+    long long b = __double2ll_rz(__dmul_rn(p, F));
+    return (uint32_t)(b < f - 1 ? b : f - 1);
+}
+__device__ __forceinline__ uint32_t bucket1(double p, double F2, int f, uint32_t parent) {
+    long long b = __double2ll_rz(__dmul_rn(p, F2)) - (long long)parent * f;
+    b = b < 0 ? 0 : b;
+    return (uint32_t)(b > f - 1 ? f - 1 : b);
+}
+// Alg.2 P:188-190 (R5): pos = clamp(floor((p - adj) * n), 0, n'-1)
+__device__ __forceinline__ uint32_t cs_pos(double p, double adj, double nd, double top) {
+    double v = floor(__dmul_rn(__dsub_rn(p, adj), nd));
+    return (uint32_t)__double2ll_rz(clampd(v, 0.0, top));
+}
+
+// ------------------------------------------------------------ control -----
+enum {
+    ST_H0B = 0, ST_H0K, ST_H1S, ST_H1K, ST_SMALLS, ST_SMALLK, ST_BIGS, ST_BIGK, ST_MAXGRP,
+    ST_BIGPASS, ST_NUM
+};
+enum { STATUS_NAN = 1u, STATUS_INTERNAL = 2u };
+constexpr int BIG_LEVELS = 6;
+
+struct Ctl {
+    uint32_t status;
+    uint32_t ticket0, ticket1, U1;
+    uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
+    uint32_t big_next[BIG_LEVELS + 1]; // work counters
+    unsigned long long smin, smax;     // finite sample ord min / max
+    unsigned long long stat[ST_NUM];
+};
+
+// Big-path work item: a key range that must be sorted exactly.
+struct BigItem {
+    uint32_t off, size;  // global key offset, size
+    uint32_t in_b;       // 1: the keys currently sit in B (else in A)
+    uint32_t g;          // originating sub-bucket (for H1 dumps), or ~0u
+};
+
+// All device pointers of one call (passed by value to kernels).
+struct Args {
+    uint64_t *A;  // keys (in place)
+    uint64_t *B;  // scratch copy
+    uint64_t n;
+    int f;        // fanout
+    int L;
+    double F, F2, nd;
+    uint32_t C0, C1;   // level-0 / level-1 unit sizes (keys)
+    uint32_t U0, U1max;
+    uint32_t T_small;  // big threshold
+    uint32_t T_tile;   // bucketsort window
+    uint32_t ntiles;
+    uint32_t big_cap;  // items per big level list
+    Ctl *ctl;
+    DevModel *M;
+    uint64_t *S;                      // sample
+    uint32_t *leaf_cnt;               // [L]
+    unsigned long long *leaf_min;     // [L]
+    unsigned long long *hist0;        // [f]
+    unsigned long long *start0;       // [f+1]
+    unsigned long long *bmin0, *bmax0;// [f]
+    uint32_t *unit1_start;            // [f+1]
+    unsigned long long *lb0;          // [U0*f]
+    uint32_t *offs0;                  // [U0*f]
+    unsigned long long *lb1;          // [U1max*f]
+    uint32_t *offs1;                  // [U1max*f]
+    uint32_t *hist1;                  // [f*f]
+    uint32_t *start1;                 // [f*f]
+    uint32_t *tile_first, *tile_last; // [ntiles]
+    BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
+    // parity dumps (may be null)
+    uint8_t *dH0, *dH1;
+};
+
+// ------------------------------------------------------------ scans -------
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// In-place exclusive scan of s[0..len) by the whole block; returns the total.
+// `tmp` must hold 33 uint32. All threads must call it.
+__device__ __forceinline__ uint32_t block_exscan(uint32_t *s, int len, uint32_t *tmp) {
+    const int per = (len + blockDim.x - 1) / blockDim.x;
+    const int beg = threadIdx.x * per;
+    uint32_t local = 0;
+    for (int i = 0; i < per; i++)
+        if (beg + i < len) local += s[beg + i];
+    uint32_t incl = warp_incl_scan(local);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if (lane == 31) tmp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = lane < nw ? tmp[lane] : 0;
+        uint32_t vi = warp_incl_scan(v);
+        if (lane < nw) tmp[lane] = vi - v;
+        if (lane == 31) tmp[32] = vi;  // total (nw <= 32)
+    }
+    __syncthreads();
+    uint32_t run = tmp[w] + incl - local;
+    for (int i = 0; i < per; i++) {
+        if (beg + i < len) {
+            uint32_t v = s[beg + i];
+            s[beg + i] = run;
+            run += v;
+        }
+    }
+    uint32_t total = tmp[32];
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *(const volatile unsigned long long *)p;
+}
+__device__ __forceinline__ void st_volatile(unsigned long long *p, unsigned long long v) {
+    *(volatile unsigned long long *)p = v;
+}
+
+}  // namespace ls

@@ -1,0 +1,195 @@
+// ls_fit.cu -- north_star (1): strided sample + two-level linear RMI fit in fp64.
+//
+// The chord model (R7) only needs, per leaf l, the number
+// of sample keys routed to it and its smallest key: the eCDF target of a leaf's
+// first key is (#sample keys in leaves < l)/m (R8: equal keys share a leaf, so
+// the strict-less rank of the leaf's first key is exactly that count). So the
+// fit is a reduction + histogram + one 1000-entry scan -- no sample sort -- and
+// its parameters are bit-identical to the oracle's (no floating-point
+// reductions are involved).
+#include "ls_launch.h"
+
+namespace ls {
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_sample_minmax(const uint64_t *__restrict__ src,
+                                                       uint64_t stride, uint64_t m,
+                                                       uint64_t *__restrict__ S, Ctl *ctl) {
+    unsigned long long mn = ~0ull, mx = 0;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gs) {
+        uint64_t b = src[k * stride];
+        if (S) S[k] = b;
+        if (is_finite_key<DT>(b) && !(DT == DT_F64 && is_nan_bits(b))) {
+            unsigned long long o = to_ord<DT>(b);
+            mn = o < mn ? o : mn;
+            mx = o > mx ? o : mx;
+        }
+    }
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (mn != ~0ull) atomicMin(&ctl->smin, mn);
+        if (mx != 0) atomicMax(&ctl->smax, mx);
+    }
+}
+
+// Root of the chord model from the finite sample range (O2).
+template <int DT>
+__device__ __forceinline__ bool fit_root(const Ctl *ctl, int L, Root &R, double &v) {
+    unsigned long long smin = ctl->smin, smax = ctl->smax;
+    if (smin > smax) {  // no finite sample key
+        v = 0.0;
+        return false;
+    }
+    R.xmin = xd<DT>(from_ord<DT>(smin));
+    R.xmax = xd<DT>(from_ord<DT>(smax));
+    v = R.xmin;
+    if (R.xmin == R.xmax) return false;
+    R.rs = __ddiv_rn((double)L, __dsub_rn(R.xmax, R.xmin));
+    R.last = (double)(L - 1);
+    R.Lm1 = L - 1;
+    return true;
+}
+
+// O3: route every sample key to its leaf; per-leaf count and smallest ord.
+template <int DT>
+__global__ void __launch_bounds__(512) k_fit_hist(const uint64_t *__restrict__ S, uint64_t m, int L,
+                                                  const Ctl *ctl, uint32_t *leaf_cnt,
+                                                  unsigned long long *leaf_min) {
+    __shared__ uint32_t cnt[LS_MAX_LEAVES];
+    __shared__ unsigned long long mn[LS_MAX_LEAVES];
+    Root R;
+    double v;
+    if (!fit_root<DT>(ctl, L, R, v)) return;  // degenerate model: nothing to fit
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        cnt[l] = 0;
+        mn[l] = ~0ull;
+    }
+    __syncthreads();
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gs) {
+        uint64_t b = S[k];
+        double xc = clampd(xd<DT>(b), R.xmin, R.xmax);
+        double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+        int l = (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+        atomicAdd(&cnt[l], 1u);
+        atomicMin(&mn[l], (unsigned long long)to_ord<DT>(b));
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        if (cnt[l]) {
+            atomicAdd(&leaf_cnt[l], cnt[l]);
+            atomicMin(&leaf_min[l], mn[l]);
+        }
+    }
+}
+
+// O4-O5: one block of 1024 threads. beg_l = #keys in leaves < l; the next
+// non-empty leaf nx(l) supplies (x1, y1); the last one runs to (xmax, PMAX).
+template <int DT>
+__global__ void __launch_bounds__(1024) k_fit_params(uint64_t m, int L, const Ctl *ctl,
+                                                     const uint32_t *leaf_cnt,
+                                                     const unsigned long long *leaf_min,
+                                                     DevModel *M) {
+    __shared__ uint32_t beg[LS_MAX_LEAVES];
+    __shared__ int nxt[LS_MAX_LEAVES + 1];
+    __shared__ uint32_t tmp[33];
+    Root R;
+    double v;
+    const bool ok = fit_root<DT>(ctl, L, R, v);
+    const int t = threadIdx.x;
+    if (t == 0) {
+        M->L = (uint32_t)L;
+        M->n_sample = m;
+        M->last = (double)(L - 1);
+        M->degenerate = ok ? 0u : 1u;
+        M->xmin = ok ? R.xmin : v;
+        M->xmax = ok ? R.xmax : v;
+        M->root_scale = ok ? R.rs : 0.0;
+    }
+    if (!ok) {  // degenerate model: p == 0
+        for (int l = t; l < L; l += blockDim.x)
+            for (int q = 0; q < 5; q++) M->leaf[5 * l + q] = 0.0;
+        return;
+    }
+    for (int l = t; l < L; l += blockDim.x) beg[l] = leaf_cnt[l];
+    __syncthreads();
+    block_exscan(beg, L, tmp);
+    // nxt[l] = smallest non-empty leaf index > l (or L): suffix minimum
+    for (int l = t; l <= L; l += blockDim.x) nxt[l] = (l < L && leaf_cnt[l] > 0) ? l : L;
+    __syncthreads();
+    for (int d = 1; d <= L; d <<= 1) {
+        int val[2];
+        int c = 0;
+        for (int l = t; l <= L && c < 2; l += blockDim.x, c++)
+            val[c] = (l + d <= L) ? min(nxt[l], nxt[l + d]) : nxt[l];
+        __syncthreads();
+        c = 0;
+        for (int l = t; l <= L && c < 2; l += blockDim.x, c++) nxt[l] = val[c];
+        __syncthreads();
+    }
+    const double md = __ull2double_rn(m);
+    for (int l = t; l < L; l += blockDim.x) {
+        const int nx = nxt[l + 1];
+        double x1, y1;
+        if (nx < L) {
+            x1 = clampd(xd<DT>(from_ord<DT>(leaf_min[nx])), R.xmin, R.xmax);
+            y1 = __ddiv_rn(__ull2double_rn(beg[nx]), md);
+        } else {
+            x1 = R.xmax;
+            y1 = PMAX;
+        }
+        const double hi = (y1 < PMAX) ? y1 : PMAX;
+        double *q = &M->leaf[5 * l];
+        if (leaf_cnt[l] > 0) {
+            double x0 = clampd(xd<DT>(from_ord<DT>(leaf_min[l])), R.xmin, R.xmax);
+            double y0 = __ddiv_rn(__ull2double_rn(beg[l]), md);
+            q[0] = (x1 > x0) ? __ddiv_rn(__dsub_rn(y1, y0), __dsub_rn(x1, x0)) : 0.0;
+            q[1] = x0;
+            q[2] = y0;
+            q[3] = y0;
+            q[4] = hi;
+        } else {
+            q[0] = 0.0;
+            q[1] = 0.0;
+            q[2] = hi;
+            q[3] = hi;
+            q[4] = hi;
+        }
+    }
+}
+
+static int grid_for(uint64_t m, int block) {
+    uint64_t g = (m + block - 1) / block;
+    if (g > 148 * 8) g = 148 * 8;
+    return g ? (int)g : 1;
+}
+
+void launch_sample_minmax(const uint64_t *src, uint64_t stride, uint64_t m, uint64_t *S_out,
+                          Ctl *ctl, int dtype, cudaStream_t st) {
+    int g = grid_for(m, 256);
+    if (dtype == DT_F64)
+        k_sample_minmax<DT_F64><<<g, 256, 0, st>>>(src, stride, m, S_out, ctl);
+    else
+        k_sample_minmax<DT_U64><<<g, 256, 0, st>>>(src, stride, m, S_out, ctl);
+}
+
+void launch_fit_hist(const uint64_t *S, uint64_t m, int L, Ctl *ctl, uint32_t *leaf_cnt,
+                     unsigned long long *leaf_min, int dtype, cudaStream_t st) {
+    int g = grid_for(m, 512 * 8);
+    if (dtype == DT_F64)
+        k_fit_hist<DT_F64><<<g, 512, 0, st>>>(S, m, L, ctl, leaf_cnt, leaf_min);
+    else
+        k_fit_hist<DT_U64><<<g, 512, 0, st>>>(S, m, L, ctl, leaf_cnt, leaf_min);
+}
+
+void launch_fit_params(uint64_t m, int L, Ctl *ctl, const uint32_t *leaf_cnt,
+                       const unsigned long long *leaf_min, DevModel *M, int dtype, cudaStream_t st) {
+    if (dtype == DT_F64)
+        k_fit_params<DT_F64><<<1, 1024, 0, st>>>(m, L, ctl, leaf_cnt, leaf_min, M);
+    else
+        k_fit_params<DT_U64><<<1, 1024, 0, st>>>(m, L, ctl, leaf_cnt, leaf_min, M);
+}
+
+}  // namespace ls

@@ -1,0 +1,399 @@
+// ls_multi.cu -- SURVEY §8(e): sample-based global range split across GPUs.
+//
+// The paper is sequential (P:414 leaves parallel execution to future work);
+// this is the multi-GPU extension named by north_star: every rank samples its
+// shard, the samples are all-gathered (NCCL), R-1 splitters are chosen on the
+// lexicographic key (ord(x), rank, index) -- so runs of equal keys may
+// straddle ranks and a heavy duplicate cannot overload one rank -- each key is
+// routed to its destination rank by a count + decoupled-lookback + scatter
+// pass (the same machinery as a partition round, with R buckets), the shards
+// are exchanged with a grouped NCCL send/recv all-to-all over NVLink, and each
+// rank sorts what it received with the single-GPU path (local model refit).
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ls.h"
+#include "ls_api_internal.h"
+#include "ls_launch.h"
+#include "ls_tile.cuh"
+
+struct ls_comm {
+    ncclComm_t comm;
+    int rank, world;
+};
+
+namespace ls {
+
+constexpr int SPLIT_K = 4096;        // sample entries per rank
+constexpr uint32_t MULTI_UNIT = 65536;
+constexpr int MAX_WORLD = 64;
+
+struct Tagged {
+    unsigned long long ord;
+    uint32_t rank, pad;
+    unsigned long long index;
+};
+static_assert(sizeof(Tagged) == sizeof(ls_tagged), "tagged layout");
+
+// Destination of (o, r, i): the number of splitters strictly below it in the
+// lexicographic order (ord, rank, index). Monotone, so rank p receives a
+// contiguous slice of the global order.
+__host__ __device__ __forceinline__ int dest_of(const Tagged *spl, int world,
+                                                unsigned long long o, uint32_t r,
+                                                unsigned long long i) {
+    int d = 0;
+    for (int k = 0; k < world - 1; k++) {
+        const Tagged &s = spl[k];
+        const bool below = s.ord < o || (s.ord == o && (s.rank < r || (s.rank == r && s.index < i)));
+        d += below ? 1 : 0;
+    }
+    return d;
+}
+
+template <int DT>
+__global__ void k_split_sample(const uint64_t *__restrict__ in, uint64_t n, uint32_t rank,
+                               Tagged *out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= SPLIT_K) return;
+    Tagged t;
+    const uint64_t valid = n < (uint64_t)SPLIT_K ? n : (uint64_t)SPLIT_K;
+    if ((uint64_t)k < valid) {
+        const uint64_t idx = n <= (uint64_t)SPLIT_K ? (uint64_t)k : (uint64_t)k * n / SPLIT_K;
+        const uint64_t b = in[idx];
+        t.ord = to_ord<DT>(b);
+        t.rank = rank;
+        t.pad = 0;
+        t.index = idx;
+    } else {
+        t.ord = ~0ull;
+        t.rank = 0xffffffffu;
+        t.pad = 0;
+        t.index = ~0ull;
+    }
+    out[k] = t;
+}
+
+struct MultiArgs {
+    const uint64_t *in;
+    uint64_t *send;
+    uint64_t n;
+    uint32_t rank;
+    int world;
+    uint32_t U;
+    const Tagged *spl;              // [world-1]
+    unsigned long long *lb;         // [U*world]
+    uint32_t *offs;                 // [U*world]
+    unsigned long long *counts;     // [world] + status
+    const unsigned long long *sdispl; // [world]
+    uint32_t *ticket;
+};
+
+template <int DT>
+struct DestBucket {
+    const Tagged *spl;
+    int world;
+    uint32_t rank;
+    __device__ __forceinline__ uint32_t operator()(uint64_t key, uint64_t idx) const {
+        return (uint32_t)dest_of(spl, world, to_ord<DT>(key), rank, idx);
+    }
+};
+
+template <int DT>
+__global__ void __launch_bounds__(512) k_dest_count(MultiArgs a) {
+    __shared__ Tagged spl[MAX_WORLD];
+    __shared__ uint32_t hist[MAX_WORLD];
+    __shared__ uint32_t s_unit;
+    __shared__ int s_nan;
+    const int tid = threadIdx.x, bd = blockDim.x, R = a.world;
+    if (tid == 0) {
+        s_unit = atomicAdd(a.ticket, 1u);
+        s_nan = 0;
+    }
+    if (tid < R - 1) spl[tid] = a.spl[tid];
+    if (tid < R) hist[tid] = 0;
+    __syncthreads();
+    const uint64_t u = s_unit;
+    const uint64_t beg = u * MULTI_UNIT, end = umin64(a.n, beg + MULTI_UNIT);
+    bool nan = false;
+    for (uint64_t i = beg + tid; i < end; i += bd) {
+        const uint64_t key = a.in[i];
+        if (DT == DT_F64 && is_nan_bits(key)) nan = true;
+        atomicAdd(&hist[dest_of(spl, R, to_ord<DT>(key), a.rank, i)], 1u);
+    }
+    if (nan) s_nan = 1;
+    __syncthreads();
+    if (tid == 0 && s_nan) atomicOr((unsigned int *)&a.counts[R], 1u);
+    for (int b = tid; b < R; b += bd) {
+        const uint32_t c = hist[b];
+        if (c) atomicAdd(&a.counts[b], (unsigned long long)c);
+        a.offs[u * R + b] = lookback(a.lb, u, 0, R, b, c);
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(512) k_dest_scatter(MultiArgs a) {
+    constexpr int KPT = 8;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ Tagged spl[MAX_WORLD];
+    __shared__ uint32_t base[MAX_WORLD], cnt[MAX_WORLD], tst[MAX_WORLD], tmp[36];
+    uint64_t *skeys = (uint64_t *)smem_raw;
+    uint16_t *sbin = (uint16_t *)(skeys + KPT * blockDim.x);
+    const int tid = threadIdx.x, R = a.world;
+    const uint64_t u = blockIdx.x;
+    if (tid < R - 1) spl[tid] = a.spl[tid];
+    if (tid < R) base[tid] = (uint32_t)a.sdispl[tid] + a.offs[u * R + tid];
+    __syncthreads();
+    const uint64_t beg = u * MULTI_UNIT, end = umin64(a.n, beg + MULTI_UNIT);
+    const DestBucket<DT> bf{spl, R, a.rank};
+    tile_scatter<KPT>(a.in, a.send, beg, end, base, cnt, tst, skeys, sbin, tmp, R, bf);
+}
+
+static bool tagged_lt(const ls_tagged &x, const ls_tagged &y) {
+    if (x.ord != y.ord) return x.ord < y.ord;
+    if (x.rank != y.rank) return x.rank < y.rank;
+    return x.index < y.index;
+}
+
+static size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+struct MultiLayout {
+    size_t send, samp, gath, spl, lb, offs, counts, allcounts, sdispl, ticket, local, total;
+    uint32_t U;
+};
+
+static MultiLayout multi_layout(uint64_t n_in, uint64_t out_cap, int R, const ls_config &cfg) {
+    MultiLayout l;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = al(off); off = o + b; return o; };
+    l.U = (uint32_t)((n_in + MULTI_UNIT - 1) / MULTI_UNIT);
+    if (l.U == 0) l.U = 1;
+    l.ticket = take(256);
+    l.counts = take((size_t)(R + 2) * 8);
+    l.lb = take((size_t)l.U * R * 8);
+    const size_t zero_end = off;
+    (void)zero_end;
+    l.send = take((size_t)n_in * 8);
+    l.samp = take((size_t)SPLIT_K * sizeof(Tagged));
+    l.gath = take((size_t)SPLIT_K * R * sizeof(Tagged));
+    l.spl = take((size_t)MAX_WORLD * sizeof(Tagged));
+    l.offs = take((size_t)l.U * R * 4);
+    l.allcounts = take((size_t)(R + 2) * R * 8);
+    l.sdispl = take((size_t)R * 8);
+    l.local = al(off);
+    l.total = l.local + workspace_bytes(out_cap > 1 ? out_cap : 2, cfg);
+    return l;
+}
+
+}  // namespace ls
+
+using namespace ls;
+
+#define NCCL_CHECK(call)                                                  \
+    do {                                                                  \
+        ncclResult_t r_ = (call);                                         \
+        if (r_ != ncclSuccess) {                                          \
+            set_error(ncclGetErrorString(r_));                            \
+            return LS_E_NCCL;                                             \
+        }                                                                 \
+    } while (0)
+#define CUDA_CHECK(call)                                                  \
+    do {                                                                  \
+        cudaError_t e_ = (call);                                          \
+        if (e_ != cudaSuccess) {                                          \
+            set_error(cudaGetErrorString(e_));                            \
+            return LS_E_CUDA;                                             \
+        }                                                                 \
+    } while (0)
+
+extern "C" {
+
+ls_status ls_multi_splitters(ls_tagged *h_entries, uint64_t count, int world, ls_tagged *h_splitters) {
+    if (world < 1 || world > MAX_WORLD || (count && !h_entries) || (world > 1 && !h_splitters)) {
+        set_error("bad arguments");
+        return LS_E_INVALID;
+    }
+    std::sort(h_entries, h_entries + count, tagged_lt);
+    uint64_t valid = 0;  // sentinel entries (rank 0xffffffff) sort last
+    while (valid < count && h_entries[valid].rank != 0xffffffffu) valid++;
+    for (int k = 1; k < world; k++) {
+        if (valid == 0) {
+            h_splitters[k - 1].ord = ~0ull;
+            h_splitters[k - 1].rank = 0xffffffffu;
+            h_splitters[k - 1].pad = 0;
+            h_splitters[k - 1].index = ~0ull;
+        } else {
+            h_splitters[k - 1] = h_entries[(uint64_t)k * valid / (uint64_t)world];
+        }
+    }
+    return LS_OK;
+}
+
+ls_status ls_multi_plan(const uint64_t *h_counts, int world, int rank, uint64_t *h_send_displ,
+                        uint64_t *h_recv_counts, uint64_t *h_recv_displ, uint64_t *n_out) {
+    if (world < 1 || rank < 0 || rank >= world || !h_counts) { set_error("bad arguments"); return LS_E_INVALID; }
+    uint64_t s = 0;
+    for (int p = 0; p < world; p++) {
+        if (h_send_displ) h_send_displ[p] = s;
+        s += h_counts[(uint64_t)rank * world + p];
+    }
+    uint64_t r = 0;
+    for (int p = 0; p < world; p++) {
+        const uint64_t c = h_counts[(uint64_t)p * world + rank];
+        if (h_recv_counts) h_recv_counts[p] = c;
+        if (h_recv_displ) h_recv_displ[p] = r;
+        r += c;
+    }
+    if (n_out) *n_out = r;
+    return LS_OK;
+}
+
+int ls_multi_dest(const ls_tagged *h_splitters, int world, uint64_t ord, uint32_t rank, uint64_t index) {
+    return dest_of((const Tagged *)h_splitters, world, ord, rank, index);
+}
+
+ls_status ls_comm_unique_id(uint8_t id[LS_UNIQUE_ID_BYTES]) {
+    static_assert(sizeof(ncclUniqueId) == LS_UNIQUE_ID_BYTES, "nccl id size");
+    ncclUniqueId u;
+    NCCL_CHECK(ncclGetUniqueId(&u));
+    memcpy(id, &u, sizeof u);
+    return LS_OK;
+}
+
+ls_status ls_comm_init(const uint8_t id[LS_UNIQUE_ID_BYTES], int rank, int world, ls_comm **out) {
+    if (!out || world < 1 || world > MAX_WORLD || rank < 0 || rank >= world) { set_error("bad arguments"); return LS_E_INVALID; }
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof u);
+    ls_comm *c = new ls_comm();
+    c->rank = rank;
+    c->world = world;
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) {
+        set_error(ncclGetErrorString(r));
+        delete c;
+        return LS_E_NCCL;
+    }
+    *out = c;
+    return LS_OK;
+}
+
+void ls_comm_destroy(ls_comm *comm) {
+    if (!comm) return;
+    ncclCommDestroy(comm->comm);
+    delete comm;
+}
+
+ls_status ls_multi_workspace_bytes(uint64_t n_in, uint64_t out_cap, int world, ls_dtype dtype,
+                                   const ls_config *cfg_in, size_t *bytes) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    if (!bytes || world < 1 || world > MAX_WORLD || (dtype != LS_F64 && dtype != LS_U64)) return LS_E_INVALID;
+    *bytes = multi_layout(n_in, out_cap, world, cfg).total;
+    return LS_OK;
+}
+
+ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_out,
+                        uint64_t out_cap, uint64_t *n_out, ls_dtype dtype, const ls_config *cfg_in,
+                        void *d_ws, size_t ws_bytes, void *stream, ls_stats *stats) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    if (!comm || !n_out || !d_ws || (n_in && !d_in) || (out_cap && !d_out)) { set_error("null pointer"); return LS_E_INVALID; }
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    if (n_in >= (1ull << 32) || out_cap >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    const int R = comm->world, me = comm->rank;
+    const MultiLayout l = multi_layout(n_in, out_cap, R, cfg);
+    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned char *w = (unsigned char *)d_ws;
+    const int dt = (int)dtype;
+    // 1. split sample + all-gather
+    Tagged *samp = (Tagged *)(w + l.samp), *gath = (Tagged *)(w + l.gath);
+    if (dt == DT_F64) k_split_sample<DT_F64><<<(SPLIT_K + 255) / 256, 256, 0, st>>>((const uint64_t *)d_in, n_in, (uint32_t)me, samp);
+    else k_split_sample<DT_U64><<<(SPLIT_K + 255) / 256, 256, 0, st>>>((const uint64_t *)d_in, n_in, (uint32_t)me, samp);
+    NCCL_CHECK(ncclAllGather(samp, gath, SPLIT_K * sizeof(Tagged), ncclUint8, comm->comm, st));
+    std::vector<ls_tagged> h((size_t)SPLIT_K * R);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), gath, h.size() * sizeof(Tagged), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    // 2. splitters (identical on every rank: same gathered bytes, same rule)
+    std::vector<ls_tagged> spl(MAX_WORLD);
+    ls_status rc = ls_multi_splitters(h.data(), h.size(), R, spl.data());
+    if (rc != LS_OK) return rc;
+    CUDA_CHECK(cudaMemcpyAsync(w + l.spl, spl.data(), (size_t)(R > 1 ? R - 1 : 1) * sizeof(Tagged), cudaMemcpyHostToDevice, st));
+    // 3. destination counts with per-unit offsets (decoupled lookback)
+    CUDA_CHECK(cudaMemsetAsync(w + l.ticket, 0, l.send - l.ticket, st));
+    MultiArgs a;
+    a.in = (const uint64_t *)d_in;
+    a.send = (uint64_t *)(w + l.send);
+    a.n = n_in;
+    a.rank = (uint32_t)me;
+    a.world = R;
+    a.U = l.U;
+    a.spl = (const Tagged *)(w + l.spl);
+    a.lb = (unsigned long long *)(w + l.lb);
+    a.offs = (uint32_t *)(w + l.offs);
+    a.counts = (unsigned long long *)(w + l.counts);
+    a.sdispl = (const unsigned long long *)(w + l.sdispl);
+    a.ticket = (uint32_t *)(w + l.ticket);
+    if (n_in) {
+        if (dt == DT_F64) k_dest_count<DT_F64><<<l.U, 512, 0, st>>>(a);
+        else k_dest_count<DT_U64><<<l.U, 512, 0, st>>>(a);
+    }
+    // 4. all-gather [counts(R), status, out_cap] -> identical plan everywhere
+    unsigned long long *row = (unsigned long long *)(w + l.counts);
+    const unsigned long long cap = out_cap;
+    CUDA_CHECK(cudaMemcpyAsync(row + R + 1, &cap, 8, cudaMemcpyHostToDevice, st));
+    NCCL_CHECK(ncclAllGather(row, w + l.allcounts, (size_t)(R + 2), ncclUint64, comm->comm, st));
+    std::vector<uint64_t> all((size_t)(R + 2) * R), mat((size_t)R * R);
+    CUDA_CHECK(cudaMemcpyAsync(all.data(), w + l.allcounts, all.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    bool any_nan = false, any_cap = false;
+    for (int p = 0; p < R; p++) {
+        for (int q = 0; q < R; q++) mat[(size_t)p * R + q] = all[(size_t)p * (R + 2) + q];
+        any_nan |= all[(size_t)p * (R + 2) + R] != 0;
+    }
+    std::vector<uint64_t> sd(R), rcnt(R), rd(R);
+    uint64_t nout = 0;
+    for (int p = 0; p < R; p++) {
+        uint64_t np = 0;
+        ls_multi_plan(mat.data(), R, p, nullptr, nullptr, nullptr, &np);
+        if (np > all[(size_t)p * (R + 2) + R + 1]) any_cap = true;
+    }
+    ls_multi_plan(mat.data(), R, me, sd.data(), rcnt.data(), rd.data(), &nout);
+    *n_out = nout;
+    if (any_nan) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
+    if (any_cap) { set_error("out_cap smaller than the received key count on some rank"); return LS_E_CAPACITY; }
+    // 5. scatter by destination into the send buffer
+    CUDA_CHECK(cudaMemcpyAsync(w + l.sdispl, sd.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
+    if (n_in) {
+        const size_t sm = 8 * 512 * 8 + 8 * 512 * 2;
+        if (dt == DT_F64) {
+            cudaFuncSetAttribute(k_dest_scatter<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_dest_scatter<DT_F64><<<l.U, 512, sm, st>>>(a);
+        } else {
+            cudaFuncSetAttribute(k_dest_scatter<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_dest_scatter<DT_U64><<<l.U, 512, sm, st>>>(a);
+        }
+    }
+    CUDA_CHECK(cudaGetLastError());
+    // 6. all-to-all over NVLink
+    const uint64_t *send = a.send;
+    uint64_t *out = (uint64_t *)d_out;
+    NCCL_CHECK(ncclGroupStart());
+    for (int p = 0; p < R; p++) {
+        const uint64_t sc = mat[(size_t)me * R + p];
+        if (sc) NCCL_CHECK(ncclSend(send + sd[p], sc, ncclUint64, p, comm->comm, st));
+        if (rcnt[p]) NCCL_CHECK(ncclRecv(out + rd[p], rcnt[p], ncclUint64, p, comm->comm, st));
+    }
+    NCCL_CHECK(ncclGroupEnd());
+    // 7. local LearnedSort 2.0 (fresh model on the received keys)
+    Pending pend;
+    rc = enqueue_sort(out, nout, dtype, &cfg, nullptr, w + l.local, ws_bytes - l.local, st, stats, nullptr, &pend);
+    if (rc != LS_OK) return rc;
+    return finish_sort(&pend, st, stats);
+}
+
+}  // extern "C"

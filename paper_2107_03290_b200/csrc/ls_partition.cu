@@ -1,0 +1,388 @@
+// ls_partition.cu -- north_star (2): the two model-guided partition rounds.
+//
+// Alg. 1 as a GPU pass pair per round. The paper places keys into
+// fixed-capacity fragments and defragments afterwards because a separate
+// counting scan was "not insignificant" on one CPU core; on
+// B200 a counting scan costs 8 B/key at HBM speed and removes the
+// defragmentation pass entirely, so each round is:
+//   count   : predict -> per-CTA shared-memory histogram of bucket ids ->
+//             decoupled lookback across units (chained prefix, one status word
+//             per (unit, bucket) carrying flag + value) -> per-unit offsets
+//   scatter : predict again -> tile-local counting sort in shared memory ->
+//             coalesced run stores at base[bucket] (no defragmentation: every
+//             bucket is written contiguously, Fig. 3c's result directly)
+// Round 0 partitions A -> B by b0 over the whole input; round 1 partitions
+// each non-homogeneous level-0 bucket B -> A by b1 (a segmented round: units
+// never straddle buckets). Level-0 homogeneous buckets are filled
+// directly from their min key.
+#include "ls_launch.h"
+#include "ls_tile.cuh"
+
+namespace ls {
+
+// ----------------------------------------------------------------- init ----
+__global__ void k_init(Ctl *ctl) {
+    if (threadIdx.x == 0) {
+        ctl->status = 0;
+        ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
+        for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
+        ctl->smin = ~0ull;
+        ctl->smax = 0;
+        for (int i = 0; i < ST_NUM; i++) ctl->stat[i] = 0;
+    }
+}
+
+void launch_init(const Args &a, cudaStream_t st) { k_init<<<1, 32, 0, st>>>(a.ctl); }
+
+// -------------------------------------------------------------- helpers ----
+template <int DT, bool SMEM_MODEL>
+__device__ __forceinline__ double predict_any(uint64_t b, const Root &R, const double *leaf) {
+    return SMEM_MODEL ? predict<DT>(b, R, leaf) : predict_ldg<DT>(b, R, leaf);
+}
+
+// Bucket function of one partition round: level 0 -> b0, level 1 -> b1(parent).
+template <int DT, int LEVEL, bool SMEM_MODEL>
+struct ModelBucket {
+    Root R;
+    const double *leaf;
+    double F, F2;
+    int f;
+    uint32_t parent;
+    __device__ __forceinline__ uint32_t operator()(uint64_t key, uint64_t) const {
+        const double p = predict_any<DT, SMEM_MODEL>(key, R, leaf);
+        return LEVEL == 0 ? bucket0(p, F, f) : bucket1(p, F2, f, parent);
+    }
+};
+
+// --------------------------------------------------------------- round 0 ---
+template <int DT>
+__global__ void __launch_bounds__(512) k_count0(Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *leaf = (double *)smem_raw;
+    uint32_t *hist = (uint32_t *)(leaf + 5 * a.L);
+    __shared__ uint32_t s_unit;
+    __shared__ int s_nan;
+    const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
+    if (tid == 0) {
+        s_unit = atomicAdd(&a.ctl->ticket0, 1u);
+        s_nan = 0;
+    }
+    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
+    for (int b = tid; b < f; b += bd) hist[b] = 0;
+    __syncthreads();
+    const uint64_t u = s_unit;
+    const Root R = load_root(a.M);
+    const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
+    bool nan = false;
+    auto one = [&](uint64_t b) {
+        if (DT == DT_F64 && is_nan_bits(b)) nan = true;
+        const double p = predict<DT>(b, R, leaf);
+        atomicAdd(&hist[bucket0(p, a.F, f)], 1u);
+    };
+    if ((((uintptr_t)(a.A + beg)) & 15) == 0) {
+        const ulonglong2 *A2 = (const ulonglong2 *)(a.A + beg);
+        const uint64_t np = (end - beg) / 2;
+        for (uint64_t i = tid; i < np; i += bd) {
+            ulonglong2 v = A2[i];
+            one(v.x);
+            one(v.y);
+        }
+        if (((end - beg) & 1) && tid == 0) one(a.A[end - 1]);
+    } else {
+        for (uint64_t i = beg + tid; i < end; i += bd) one(a.A[i]);
+    }
+    if (nan) s_nan = 1;
+    __syncthreads();
+    if (tid == 0 && s_nan) atomicOr(&a.ctl->status, (uint32_t)STATUS_NAN);
+    for (int b = tid; b < f; b += bd) {
+        const uint32_t c = hist[b];
+        if (c) atomicAdd(&a.hist0[b], (unsigned long long)c);
+        a.offs0[u * f + b] = lookback(a.lb0, u, 0, f, b, c);
+    }
+}
+
+// S_B (Alg. 1 output), bucket starts (Alg. 2 read head) and the
+// round-1 unit plan. One block.
+__global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
+    __shared__ uint32_t s[LS_MAX_FANOUT + 1];
+    __shared__ uint32_t nu[LS_MAX_FANOUT + 1];
+    __shared__ uint32_t tmp[33];
+    const int f = a.f, tid = threadIdx.x;
+    for (int b = tid; b < f; b += blockDim.x) {
+        const uint64_t h = a.hist0[b];
+        s[b] = (uint32_t)h;
+        nu[b] = (uint32_t)((h + a.C1 - 1) / a.C1);
+        if (dS_B) dS_B[b] = h;
+    }
+    __syncthreads();
+    const uint32_t total = block_exscan(s, f, tmp);
+    const uint32_t units = block_exscan(nu, f, tmp);
+    for (int b = tid; b < f; b += blockDim.x) {
+        a.start0[b] = s[b];
+        a.unit1_start[b] = nu[b];
+    }
+    if (tid == 0) {
+        a.start0[f] = total;
+        a.unit1_start[f] = units;
+        a.ctl->U1 = units;
+        if ((uint64_t)total != a.n) atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(512) k_scatter0(Args a) {
+    if (a.ctl->status) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int KPT = 8;
+    const int f = a.f, tid = threadIdx.x, bd = blockDim.x;
+    uint64_t *skeys = (uint64_t *)smem_raw;  // [KPT*bd]
+    double *leaf = (double *)(skeys + KPT * bd);
+    uint32_t *base = (uint32_t *)(leaf + 5 * a.L);
+    uint32_t *cnt = base + f;
+    uint32_t *tst = cnt + f;
+    uint32_t *tmp = tst + f;  // 33
+    uint16_t *sbin = (uint16_t *)(tmp + 36);
+    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
+    const uint64_t u = blockIdx.x;
+    for (int b = tid; b < f; b += bd) base[b] = (uint32_t)a.start0[b] + a.offs0[u * f + b];
+    __syncthreads();
+    const Root R = load_root(a.M);
+    const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
+    const ModelBucket<DT, 0, true> bf{R, leaf, a.F, a.F2, f, 0u};
+    tile_scatter<KPT>(a.A, a.B, beg, end, base, cnt, tst, skeys, sbin, tmp, f, bf);
+}
+
+// --------------------------------------------------------------- round 1 ---
+__device__ __forceinline__ int find_bucket(const uint32_t *ustart, int f, uint32_t u) {
+    int lo = 0, hi = f - 1;  // largest b with ustart[b] <= u
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (ustart[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(512) k_count1(Args a) {
+    __shared__ uint32_t hist[LS_MAX_FANOUT];
+    __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
+    __shared__ unsigned long long s_mn[32], s_mx[32];
+    __shared__ uint32_t s_unit;
+    const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
+    if (tid == 0) s_unit = atomicAdd(&a.ctl->ticket1, 1u);
+    for (int b = tid; b <= f; b += bd) ustart[b] = a.unit1_start[b];
+    for (int b = tid; b < f; b += bd) hist[b] = 0;
+    __syncthreads();
+    const uint32_t u = s_unit;
+    if (u >= a.ctl->U1 || a.ctl->status) return;
+    const int b = find_bucket(ustart, f, u);
+    const uint32_t slice = u - ustart[b];
+    const uint64_t bend = a.start0[b + 1];
+    const uint64_t beg = a.start0[b] + (uint64_t)slice * a.C1;
+    const uint64_t end = umin64(bend, beg + a.C1);
+    const Root R = load_root(a.M);
+    unsigned long long mn = ~0ull, mx = 0;
+    for (uint64_t i = beg + tid; i < end; i += bd) {
+        const uint64_t key = a.B[i];
+        const unsigned long long o = to_ord<DT>(key);
+        mn = o < mn ? o : mn;
+        mx = o > mx ? o : mx;
+        const double p = predict_ldg<DT>(key, R, a.M->leaf);
+        atomicAdd(&hist[bucket1(p, a.F2, f, (uint32_t)b)], 1u);
+    }
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    if ((tid & 31) == 0) {
+        s_mn[tid >> 5] = mn;
+        s_mx[tid >> 5] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < (bd + 31) / 32; w++) {
+            mn = s_mn[w] < mn ? s_mn[w] : mn;
+            mx = s_mx[w] > mx ? s_mx[w] : mx;
+        }
+        atomicMin(&a.bmin0[b], mn);
+        atomicMax(&a.bmax0[b], mx);
+    }
+    for (int j = tid; j < f; j += bd) {
+        const uint32_t c = hist[j];
+        if (c) atomicAdd(&a.hist1[(uint64_t)b * f + j], c);
+        a.offs1[(uint64_t)u * f + j] = lookback(a.lb1, u, ustart[b], f, j, c);
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(512) k_scatter1(Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int KPT = 8;
+    __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
+    const int f = a.f, tid = threadIdx.x, bd = blockDim.x;
+    const uint32_t u = blockIdx.x;
+    if (u >= a.ctl->U1 || a.ctl->status) return;
+    uint64_t *skeys = (uint64_t *)smem_raw;  // [KPT*bd]
+    uint32_t *base = (uint32_t *)(skeys + KPT * bd);
+    uint32_t *cnt = base + f;
+    uint32_t *tst = cnt + f;
+    uint32_t *tmp = tst + f;
+    uint16_t *sbin = (uint16_t *)(tmp + 36);
+    for (int b = tid; b <= f; b += bd) ustart[b] = a.unit1_start[b];
+    __syncthreads();
+    const int b = find_bucket(ustart, f, u);
+    const uint32_t slice = u - ustart[b];
+    const uint64_t bbeg = a.start0[b], bend = a.start0[b + 1];
+    const uint64_t beg = bbeg + (uint64_t)slice * a.C1;
+    const uint64_t end = umin64(bend, beg + a.C1);
+    const unsigned long long mn = a.bmin0[b];
+    if (bend - bbeg <= 1 || mn == a.bmax0[b]) {
+        // homogeneous level-0 bucket: already in final position
+        // after defragmentation; here it is written straight from its value.
+        const uint64_t v = from_ord<DT>(mn);
+        for (uint64_t i = beg + tid; i < end; i += bd) a.A[i] = v;
+        return;
+    }
+    for (int j = tid; j < f; j += bd) tst[j] = a.hist1[(uint64_t)b * f + j];
+    __syncthreads();
+    block_exscan(tst, f, tmp);
+    for (int j = tid; j < f; j += bd)
+        base[j] = (uint32_t)bbeg + tst[j] + a.offs1[(uint64_t)u * f + j];
+    __syncthreads();
+    const Root R = load_root(a.M);
+    const ModelBucket<DT, 1, false> bf{R, a.M->leaf, a.F, a.F2, f, (uint32_t)b};
+    tile_scatter<KPT>(a.B, a.A, beg, end, base, cnt, tst, skeys, sbin, tmp, f, bf);
+}
+
+// ------------------------------------------------------------- classify ----
+// Per level-0 bucket b (one block): H0, S'_B row, sub-bucket starts,
+// H1 for n' <= 1, SMALL -> bucket-sort tiles, BIG -> big-path list.
+__global__ void __launch_bounds__(1024) k_classify(Args a) {
+    __shared__ uint32_t s[LS_MAX_FANOUT];
+    __shared__ uint32_t tmp[33];
+    const int b = blockIdx.x, f = a.f, tid = threadIdx.x;
+    const uint64_t row = (uint64_t)b * f;
+    const uint64_t bbeg = a.start0[b], nb = a.start0[b + 1] - bbeg;
+    const bool h0 = nb <= 1 || a.bmin0[b] == a.bmax0[b];
+    if (h0) {
+        if (tid == 0) {
+            if (a.dH0) a.dH0[b] = 1;
+            if (nb >= 2) {
+                atomicAdd(&a.ctl->stat[ST_H0B], 1ull);
+                atomicAdd(&a.ctl->stat[ST_H0K], (unsigned long long)nb);
+            }
+        }
+        for (int j = tid; j < f; j += blockDim.x) {
+            a.hist1[row + j] = 0;
+            a.start1[row + j] = (uint32_t)bbeg;
+        }
+        return;
+    }
+    for (int j = tid; j < f; j += blockDim.x) s[j] = a.hist1[row + j];
+    __syncthreads();
+    const uint32_t total = block_exscan(s, f, tmp);
+    if (tid == 0 && total != nb) atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+    for (int j = tid; j < f; j += blockDim.x) {
+        const uint64_t g = row + j;
+        const uint32_t c = a.hist1[g];
+        const uint32_t st = (uint32_t)bbeg + s[j];
+        a.start1[g] = st;
+        if (c <= 1) {
+            if (a.dH1) a.dH1[g] = 1;
+        } else if (c <= a.T_small) {
+            const uint32_t t = st / a.T_tile;
+            atomicMin(&a.tile_first[t], (uint32_t)g);
+            atomicMax(&a.tile_last[t], (uint32_t)g);
+        } else {
+            const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
+            if (k < a.big_cap) a.big[k] = BigItem{st, c, 0u, (uint32_t)g};
+            else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+        }
+    }
+}
+
+// ---------------------------------------------------------- parity hooks ---
+template <int DT>
+__global__ void k_bucket_ids(const uint64_t *__restrict__ keys, uint64_t n, int f,
+                             const DevModel *M, double *p_out, uint32_t *b0_out, uint32_t *b1_out,
+                             unsigned long long *h0, unsigned long long *h1) {
+    const Root R = load_root(M);
+    const double F = (double)f, F2 = (double)f * (double)f;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gs) {
+        const double p = predict_ldg<DT>(keys[i], R, M->leaf);
+        const uint32_t b0 = bucket0(p, F, f), b1 = bucket1(p, F2, f, b0);
+        if (p_out) p_out[i] = p;
+        if (b0_out) b0_out[i] = b0;
+        if (b1_out) b1_out[i] = b1;
+        if (h0) atomicAdd(&h0[b0], 1ull);
+        if (h1) atomicAdd(&h1[(uint64_t)b0 * f + b1], 1ull);
+    }
+}
+
+template <int DT>
+__global__ void k_bucket_pos(const uint64_t *__restrict__ keys, uint64_t n, int f,
+                             const DevModel *M, const unsigned long long *h1, uint32_t *pos) {
+    const Root R = load_root(M);
+    const double F = (double)f, F2 = (double)f * (double)f, nd = (double)n;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gs) {
+        const double p = predict_ldg<DT>(keys[i], R, M->leaf);
+        const uint32_t b0 = bucket0(p, F, f), b1 = bucket1(p, F2, f, b0);
+        const uint64_t g = (uint64_t)b0 * f + b1;
+        const double adj = __ddiv_rn((double)g, F2);
+        pos[i] = cs_pos(p, adj, nd, (double)(h1[g] - 1));
+    }
+}
+
+// -------------------------------------------------------------- launchers --
+static size_t smem_count0(const Args &a) { return 5 * a.L * sizeof(double) + a.f * 4; }
+static size_t smem_scatter0(const Args &a) {
+    return 8 * 512 * 8 + 5 * a.L * 8 + 3 * a.f * 4 + 36 * 4 + 8 * 512 * 2;
+}
+static size_t smem_scatter1(const Args &a) { return 8 * 512 * 8 + 3 * a.f * 4 + 36 * 4 + 8 * 512 * 2; }
+
+template <class K>
+static void set_smem(K k, size_t bytes) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_count0(const Args &a, int dtype, cudaStream_t st) {
+    size_t sm = smem_count0(a);
+    if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<a.U0, 512, sm, st>>>(a); }
+    else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<a.U0, 512, sm, st>>>(a); }
+}
+void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st) { k_plan0<<<1, 1024, 0, st>>>(a, dS_B); }
+void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
+    size_t sm = smem_scatter0(a);
+    if (dtype == DT_F64) { set_smem(k_scatter0<DT_F64>, sm); k_scatter0<DT_F64><<<a.U0, 512, sm, st>>>(a); }
+    else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<a.U0, 512, sm, st>>>(a); }
+}
+void launch_count1(const Args &a, int dtype, cudaStream_t st) {
+    if (dtype == DT_F64) k_count1<DT_F64><<<a.U1max, 512, 0, st>>>(a);
+    else k_count1<DT_U64><<<a.U1max, 512, 0, st>>>(a);
+}
+void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
+    size_t sm = smem_scatter1(a);
+    if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64>, sm); k_scatter1<DT_F64><<<a.U1max, 512, sm, st>>>(a); }
+    else { set_smem(k_scatter1<DT_U64>, sm); k_scatter1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
+}
+void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st) {
+    (void)dS_B1;
+    k_classify<<<a.f, 1024, 0, st>>>(a);
+}
+void launch_bucket_ids(const uint64_t *keys, uint64_t n, int f, const DevModel *M, double *p,
+                       uint32_t *b0, uint32_t *b1, unsigned long long *h0, unsigned long long *h1,
+                       int dtype, cudaStream_t st) {
+    int g = (int)umin64((n + 255) / 256, 148 * 16);
+    if (g < 1) g = 1;
+    if (dtype == DT_F64) k_bucket_ids<DT_F64><<<g, 256, 0, st>>>(keys, n, f, M, p, b0, b1, h0, h1);
+    else k_bucket_ids<DT_U64><<<g, 256, 0, st>>>(keys, n, f, M, p, b0, b1, h0, h1);
+}
+void launch_bucket_pos(const uint64_t *keys, uint64_t n, int f, const DevModel *M,
+                       const unsigned long long *h1, uint32_t *pos, int dtype, cudaStream_t st) {
+    int g = (int)umin64((n + 255) / 256, 148 * 16);
+    if (g < 1) g = 1;
+    if (dtype == DT_F64) k_bucket_pos<DT_F64><<<g, 256, 0, st>>>(keys, n, f, M, h1, pos);
+    else k_bucket_pos<DT_U64><<<g, 256, 0, st>>>(keys, n, f, M, h1, pos);
+}
+
+}  // namespace ls

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north_star): sorted output bit-exact; with identical model parameters,
+p / b0 / b1 / pos / S_B / S'_B / H0 / H1 bit-exact; independently fitted RMI
+parameters bit-identical (the chord fit has no floating-point reductions, so
+the 1e-9 relative allowance is not needed). Inputs are generated on the device
+and the same bytes are handed to the oracle.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2107_03290_b200 as ls  # noqa: E402
+
+DEV = torch.device("cuda:0")
+DISTS_F64 = ["uniform01", "normal", "lognormal", "exponential", "mixgauss", "chisq4"]
+DISTS_U64 = ["zipf", "rootdups", "twodups", "telemetry", "uniform_u64"]
+
+
+def gen(dist, n, seed):
+    plan = datagen.Plan(dist, n, seed)
+    t = torch.empty(n, dtype=torch.float64 if plan.dtype == np.float64 else torch.uint64, device=DEV)
+    if n:
+        plan.device(t)
+    torch.cuda.synchronize()
+    return t
+
+
+def to_np(t):
+    a = t.view(torch.int64).cpu().numpy().view(np.uint64)
+    return a.view(np.float64) if t.dtype == torch.float64 else a
+
+
+def from_np(a):
+    t = torch.from_numpy(a.view(np.int64).copy()).to(DEV)
+    return t.view(torch.float64) if a.dtype == np.float64 else t.view(torch.uint64)
+
+
+def bits(x):
+    return np.ascontiguousarray(x).view(np.uint64)
+
+
+def oracle_model_to_ls(m: O.Model) -> ls.Model:
+    out = ls.Model()
+    out.leaf_count, out.n_sample, out.degenerate = m.leaf_count, m.n_sample, m.degenerate
+    out.xmin, out.xmax, out.root_scale = m.xmin, m.xmax, m.root_scale
+    C.memmove(C.addressof(out.leaf), C.addressof(m.leaf), 40 * m.leaf_count)
+    return out
+
+
+def ls_leaves(m: ls.Model) -> np.ndarray:
+    arr = np.ctypeslib.as_array(m.leaf).view(np.float64).reshape(-1, 5)
+    return arr[: m.leaf_count].copy()
+
+
+def assert_models_identical(g: ls.Model, o: O.Model):
+    assert g.leaf_count == o.leaf_count and g.degenerate == o.degenerate
+    assert g.n_sample == o.n_sample
+    for k in ("xmin", "xmax", "root_scale"):
+        assert bits(np.float64(getattr(g, k))) == bits(np.float64(getattr(o, k))), k
+    assert np.array_equal(bits(ls_leaves(g)), bits(o.leaves()))
+
+
+def dumps_for(f):
+    d = dict(S_B=torch.zeros(f, dtype=torch.int64, device=DEV),
+             S_B1=torch.zeros(f * f, dtype=torch.int32, device=DEV),
+             H0=torch.zeros(f, dtype=torch.uint8, device=DEV),
+             H1=torch.zeros(f * f, dtype=torch.uint8, device=DEV))
+    model = ls.Model()
+    dd = ls.Dumps(d["S_B"].data_ptr(), d["S_B1"].data_ptr(), d["H0"].data_ptr(),
+                  d["H1"].data_ptr(), C.pointer(model))
+    return d, dd, model
+
+
+# ------------------------------------------------------------------ model ---
+
+@pytest.mark.parametrize("dist", DISTS_F64 + DISTS_U64)
+def test_train_rmi_bit_identical(dist):
+    keys = gen(dist, 1_000_000, 3)
+    sample = keys[::100].contiguous()
+    g = ls.ls_train_rmi(sample)
+    o = O.train(to_np(sample), stride=1)
+    assert_models_identical(g, o)
+    # the fit inside ls_sort (strided sample of the whole input) == oracle's O1-O5
+    d, dd, model = dumps_for(1000)
+    ls.ls_sort(keys.clone(), dumps=dd)
+    assert_models_identical(model, O.train(to_np(keys)))
+
+
+# -------------------------------------------------------- ids / histograms --
+
+@pytest.mark.parametrize("dist", ["normal", "exponential", "mixgauss", "zipf", "twodups", "telemetry"])
+def test_bucket_ids_bit_exact(dist):
+    keys = gen(dist, 1_000_000, 5)
+    h = to_np(keys)
+    _, om, _, od = O.sort(h, dumps=True)
+    out = ls.ls_bucket_ids(keys, oracle_model_to_ls(om))
+    assert np.array_equal(bits(out["p"].cpu().numpy()), bits(od["p"]))
+    for k in ("b0", "b1", "pos"):
+        assert np.array_equal(out[k].cpu().numpy().astype(np.uint32), od[k]), k
+    assert np.array_equal(out["hist1"].cpu().numpy().astype(np.uint64), od["hist1_raw"])
+    assert np.array_equal(out["hist0"].cpu().numpy().astype(np.uint64), od["S_B"])
+
+
+# ------------------------------------------------------------- whole sort ---
+
+def check_sort(keys, cfg=None, model=None, ocfg=None, f=1000):
+    h = to_np(keys)
+    osorted, om, ost, od = O.sort(h, cfg=ocfg, dumps=True,
+                                  model=None if model is None else model)
+    d, dd, gm = dumps_for(f)
+    t = keys.clone()
+    st = ls.ls_sort(t, cfg=cfg, dumps=dd,
+                    model=None if model is None else oracle_model_to_ls(model))
+    got = to_np(t)
+    assert np.array_equal(bits(got), bits(osorted)), "sorted output differs from the oracle"
+    assert np.array_equal(d["S_B"].cpu().numpy().astype(np.uint64), od["S_B"])
+    assert np.array_equal(d["H0"].cpu().numpy(), od["H0"])
+    assert np.array_equal(d["S_B1"].cpu().numpy().astype(np.uint64), od["S_B1"])
+    assert np.array_equal(d["H1"].cpu().numpy(), od["H1"])
+    assert st["h0_buckets"] == ost["h0_buckets"] and st["h0_keys"] == ost["h0_keys"]
+    assert st["h1_subbuckets"] == ost["h1_subbuckets"] and st["h1_keys"] == ost["h1_keys"]
+    return st, ost
+
+
+@pytest.mark.parametrize("dist", DISTS_F64 + DISTS_U64)
+def test_sort_bit_exact_1e6(dist):
+    st, ost = check_sort(gen(dist, 1_000_000, 7))
+    assert st["small_keys"] + st["big_keys"] + st["h1_keys"] + st["h0_keys"] <= 1_000_000
+
+
+@pytest.mark.parametrize("dist", ["normal", "lognormal", "zipf", "rootdups", "twodups", "telemetry"])
+def test_sort_bit_exact_1e7(dist):
+    check_sort(gen(dist, 10_000_000, 11))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 31, 99, 100, 101, 2047, 2048, 2049, 4097, 8191, 8192,
+                               8193, 65535, 65536, 65537, 131073, 300_001])
+def test_sort_sizes(n):
+    for dist in ("normal", "twodups"):
+        keys = gen(dist, n, n)
+        h = to_np(keys)
+        t = keys.clone()
+        ls.ls_sort(t)
+        want = O.sort(h)[0] if n else h
+        assert np.array_equal(bits(to_np(t)), bits(want))
+
+
+EDGE = {
+    "inf_denormal_zero": np.array([np.inf, -np.inf, 1.0, -1.0, 0.0, 5e-324, -5e-324, 1e308,
+                                   -1e308, 2.5] * 3000),
+    "signed_zero": np.array([-0.0, 0.0] * 5000 + [1.0]),
+    "all_inf": np.array([np.inf] * 500 + [-np.inf] * 500),
+    "all_equal": np.full(100_000, 3.25),
+    "two_values": np.array([1.0, 2.0] * 60_000),
+    "sorted": np.arange(200_000, dtype=np.float64),
+    "reverse": np.arange(200_000, dtype=np.float64)[::-1].copy(),
+    "u64_extremes": np.array([2 ** 64 - 1, 2 ** 64 - 2, 0, 1, 2 ** 63] * 4000, dtype=np.uint64),
+    "u64_fp64_collisions": np.array([2 ** 60 + k for k in range(50_000)][::-1], dtype=np.uint64),
+    "u64_collide_dups": np.array([2 ** 53 + k for k in range(0, 30_000, 3)] * 7, dtype=np.uint64),
+    "huge_range": np.array([-1.7e308, 1.7e308, 0.0, 1.0] * 10_000),
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_sort_edge_cases(name):
+    a = EDGE[name].copy()
+    np.random.default_rng(0).shuffle(a)
+    for stride in (1, 100):
+        cfg = ls.config(sample_stride=stride)
+        ocfg = O.config(sample_stride=stride)
+        keys = from_np(a)
+        h = to_np(keys)
+        t = keys.clone()
+        ls.ls_sort(t, cfg=cfg)
+        assert np.array_equal(bits(to_np(t)), bits(O.sort(h, cfg=ocfg)[0]))
+
+
+def test_nan_rejected_input_untouched():
+    a = np.random.default_rng(1).standard_normal(100_000)
+    a[54_321] = np.nan
+    t = from_np(a)
+    with pytest.raises(ls.LSError) as e:
+        ls.ls_sort(t)
+    assert e.value.status == ls.LS_E_NAN
+    assert np.array_equal(bits(to_np(t)), bits(a))
+
+
+def test_fault_injection_models():
+    """constant model / zero slopes / foreign model still sort exactly."""
+    keys = gen("lognormal", 300_000, 13)
+    h = to_np(keys)
+    const = O.Model()
+    const.leaf_count, const.n_sample = 1, 1
+    const.leaf[0].a, const.leaf[0].b, const.leaf[0].lo, const.leaf[0].hi = 0.0, 0.3, 0.3, 0.3
+    foreign = O.train(datagen.generate_host("normal", 300_000, 1))
+    flat = O.train(h)
+    for l in range(flat.leaf_count):
+        flat.leaf[l].a = 0.0
+    for m in (const, foreign, flat):
+        check_sort(keys, model=m)
+
+
+def test_injected_model_validation():
+    keys = gen("normal", 10_000, 1)
+    m = oracle_model_to_ls(O.train(to_np(keys)))
+    m.leaf[3].a = -1.0
+    with pytest.raises(ls.LSError) as e:
+        ls.ls_sort(keys.clone(), model=m)
+    assert e.value.status == ls.LS_E_INVALID
+
+
+@pytest.mark.parametrize("f,L,stride,n", [(2, 1000, 1, 5000), (3, 7, 2, 20_000), (10, 50, 5, 100_000),
+                                          (64, 1000, 100, 500_000), (1024, 1024, 100, 2_000_000)])
+def test_other_fanouts(f, L, stride, n):
+    keys = gen("exponential", n, f)
+    check_sort(keys, cfg=ls.config(fanout=f, leaf_count=L, sample_stride=stride),
+               ocfg=O.config(fanout=f, leaf_count=L, sample_stride=stride), f=f)
+
+
+@pytest.mark.parametrize("thr", [64, 512, 4096])
+def test_big_threshold(thr):
+    """Small thresholds push sub-buckets through the exact big path."""
+    for dist in ("telemetry", "normal"):
+        keys = gen(dist, 1_000_000, 17)
+        h = to_np(keys)
+        t = keys.clone()
+        st = ls.ls_sort(t, cfg=ls.config(big_threshold=thr))
+        assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
+        if thr == 64:
+            assert st["big_subbuckets"] > 0
+
+
+def test_sort_host_end_to_end():
+    keys = gen("mixgauss", 2_000_000, 23)
+    h = to_np(keys)
+    host = torch.from_numpy(h.copy()).pin_memory()
+    buf = torch.empty_like(keys)
+    ls.ls_sort_host(host, buf)
+    assert np.array_equal(bits(host.numpy()), bits(np.sort(h)))
+
+
+def test_determinism():
+    keys = gen("twodups", 3_000_000, 29)
+    outs = []
+    for _ in range(2):
+        d, dd, _ = dumps_for(1000)
+        t = keys.clone()
+        ls.ls_sort(t, dumps=dd)
+        outs.append((to_np(t), {k: v.cpu().numpy() for k, v in d.items()}))
+    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k])
+
+
+# --------------------------------------------------------- full size (200M) -
+
+def splitmix(o):
+    z = o + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dist", ["normal", "zipf", "telemetry", "twodups"])
+def test_full_size_200m(dist):
+    """BASELINE configs 2-4 at full size in the bench launch configuration:
+    model bit-identical to the oracle's fit on the same 200M keys, p/b0/b1 on
+    10^5 sampled keys bit-exact, output sorted, multiset hash preserved,
+    S_B = run lengths of b0 along the sorted output."""
+    n = 200_000_000
+    keys = gen(dist, n, 0 if dist != "zipf" else 1)
+    h = to_np(keys)
+    om = O.train(h)
+    d, dd, gm = dumps_for(1000)
+    t = keys.clone()
+    ws = ls.workspace(n, ls.dtype_code(t))
+    ls.ls_sort(t, ws=ws, dumps=dd)
+    assert_models_identical(gm, om)
+    idx = np.random.default_rng(0).choice(n, 100_000, replace=False)
+    sub = from_np(h[idx])
+    ids = ls.ls_bucket_ids(sub, oracle_model_to_ls(om), want=("p", "b0", "b1"))
+    p = O.predict(om, h[idx])
+    assert np.array_equal(bits(ids["p"].cpu().numpy()), bits(p))
+    b0 = np.minimum((p * 1000).astype(np.int64), 999)
+    assert np.array_equal(ids["b0"].cpu().numpy(), b0)
+    got = to_np(t)
+    o = O.ord_key(got)
+    assert np.all(o[1:] >= o[:-1])
+    oi = O.ord_key(h)
+    sh, sg = splitmix(oi), splitmix(o)
+    assert np.bitwise_xor.reduce(sh) == np.bitwise_xor.reduce(sg)
+    assert sh.sum(dtype=np.uint64) == sg.sum(dtype=np.uint64)
+    del sh, sg, oi
+    gb0 = ls.ls_bucket_ids(t, gm, ws=ws, want=("hist0",))["hist0"].cpu().numpy()
+    assert np.array_equal(gb0, d["S_B"].cpu().numpy())
