@@ -60,7 +60,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -234,9 +234,9 @@ def run_ours(args):
     # correctness guard on the last step (cheap, on device): output non-decreasing
     res = (out[: n_out] if multi else keys)
     u = res.view(torch.int64)
-    if res.dtype == torch.float64:
-        o = torch.where(u < 0, ~u, u ^ torch.iinfo(torch.int64).min)
-    else:
+    if res.dtype == torch.float64:  # totalOrder as a signed key: flip magnitude bits of negatives
+        o = torch.where(u < 0, u ^ torch.iinfo(torch.int64).max, u)
+    else:  # unsigned order as a signed key: flip the top bit
         o = u ^ torch.iinfo(torch.int64).min
     sorted_ok = bool((o[1:] >= o[:-1]).all().item())
 

@@ -39,7 +39,8 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        lb1, offs1, hist1, start1, tfirst, tlast, big, hist1_u64, B;
+        lb1, offs1, hist1, start1, tfirst, tlast, tdesc, big, chunks, hist1_u64, B;
+    uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
 
@@ -90,7 +91,10 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.offs0 = take((size_t)l.U0 * l.f * 4);
     l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
+    l.tdesc = take((size_t)l.ntiles * 16);
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
+    l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
+    l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
     l.hist1_u64 = take(ff * 8);
     l.B = take((size_t)n * 8);
     l.total = align_up(off, 256);
@@ -135,7 +139,10 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.start1 = (uint32_t *)(w + l.start1);
     a.tile_first = (uint32_t *)(w + l.tfirst);
     a.tile_last = (uint32_t *)(w + l.tlast);
+    a.tdesc = (uint4 *)(w + l.tdesc);
     a.big = (BigItem *)(w + l.big);
+    a.chunks = (BigChunk *)(w + l.chunks);
+    a.chunk_cap = l.chunk_cap;
     return a;
 }
 
@@ -144,7 +151,7 @@ static ls_status check_config(const ls_config &c) {
     if (c.leaf_count < 1 || c.leaf_count > LS_MAX_LEAVES) { set_error("leaf_count out of range [1, 1024]"); return LS_E_INVALID; }
     if (c.sample_stride < 1) { set_error("sample_stride must be >= 1"); return LS_E_INVALID; }
     if (c.fit != 0) { set_error("only the chord fit (0) is implemented"); return LS_E_INVALID; }
-    if (c.big_threshold < 64 || c.big_threshold > 4096) { set_error("big_threshold out of range [64, 4096]"); return LS_E_INVALID; }
+    if (c.big_threshold < 64 || c.big_threshold > 2048) { set_error("big_threshold out of range [64, 2048]"); return LS_E_INVALID; }
     return LS_OK;
 }
 
@@ -298,8 +305,10 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
     tm.mark(LS_PHASE_CLASSIFY);
     launch_bucketsort(a, dt, st);
-    launches++;
+    launches += 2;
     tm.mark(LS_PHASE_BUCKETSORT);
+    launch_big_minmax(a, dt, st);
+    launches++;
     for (int lv = 0; lv < BIG_LEVELS; lv++) {
         launch_big(a, lv, dt, st);
         launches++;
@@ -446,8 +455,7 @@ ls_status ls_train_rmi(const void *d_sample, uint64_t m, ls_dtype dtype, const l
     if (!out || !d_ws || (m && !d_sample)) { set_error("null pointer"); return LS_E_INVALID; }
     if (m == 0) { set_error("empty sample (S:59)"); return LS_E_INVALID; }
     if (dtype != LS_F64 && dtype != LS_U64) return LS_E_INVALID;
-    cfg.sample_stride = 1;
-    const Layout l = make_layout(m, cfg);
+    const Layout l = make_layout(m, cfg);  // (the sample buffer S of the layout is unused)
     if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
     Args a = make_args(l, nullptr, d_ws);
     cudaStream_t st = (cudaStream_t)stream;

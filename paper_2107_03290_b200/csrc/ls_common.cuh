@@ -126,6 +126,7 @@ struct Ctl {
     uint32_t ticket0, ticket1, U1;
     uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
+    uint32_t nchunks;                  // k_big_minmax work entries
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
 };
@@ -135,6 +136,12 @@ struct BigItem {
     uint32_t off, size;  // global key offset, size
     uint32_t in_b;       // 1: the keys currently sit in B (else in A)
     uint32_t g;          // originating sub-bucket (for H1 dumps), or ~0u
+    unsigned long long mn, mx;  // ord range (level 0: filled by k_big_minmax)
+    uint32_t pad0, pad1;
+};
+constexpr uint32_t MM_CHUNK = 65536;
+struct BigChunk {
+    uint32_t item, chunk;
 };
 
 // All device pointers of one call (passed by value to kernels).
@@ -167,7 +174,10 @@ struct Args {
     uint32_t *hist1;                  // [f*f]
     uint32_t *start1;                 // [f*f]
     uint32_t *tile_first, *tile_last; // [ntiles]
+    uint4 *tdesc;                     // [ntiles] {g0, g1, lo, hi}
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
+    BigChunk *chunks;                 // [chunk_cap]
+    uint32_t chunk_cap;
     // parity dumps (may be null)
     uint8_t *dH0, *dH1;
 };
@@ -237,6 +247,105 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 }
 __device__ __forceinline__ void st_volatile(unsigned long long *p, unsigned long long v) {
     *(volatile unsigned long long *)p = v;
+}
+
+}  // namespace ls
+
+namespace ls {
+
+// ------------------------------------------------- TMA 1-D bulk copies ----
+// cp.async.bulk (the bulk-copy engine of the TMA unit; SASS UBLKCP) moves a
+// contiguous global range into shared memory and signals an mbarrier with the
+// byte count. Addresses 16-byte aligned, sizes multiples of 16.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(mbar)), "r"(phase)
+            : "memory");
+    }
+}
+
+// Stage global keys [glo, ghi) into smem so that key k lands at sdst[k - glo].
+// The bulk engine needs 16-byte alignment, so the copy covers the aligned hull
+// [glo & ~1, (ghi + 1) & ~1) starting at sbase; returns sbase + (glo & 1).
+// Called by all threads; thread 0 issues, everyone waits.
+__device__ __forceinline__ uint64_t *stage_keys(const uint64_t *g, uint32_t glo, uint32_t ghi,
+                                                uint64_t *sbase, uint64_t *mbar) {
+    const uint32_t alo = glo & ~1u, ahi = (ghi + 1) & ~1u;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        const uint32_t bytes = (ahi - alo) * 8u;
+        mbar_expect_tx(mbar, bytes);
+        constexpr uint32_t CH = 16384;
+        for (uint32_t o = 0; o < bytes; o += CH)
+            bulk_g2s((char *)sbase + o, (const char *)(g + alo) + o, bytes - o < CH ? bytes - o : CH, mbar);
+    }
+    __syncthreads();
+    mbar_wait(mbar, 0);
+    return sbase + (glo - alo);
+}
+
+__device__ __forceinline__ uint32_t warp_incl_max(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = t > v ? t : v;
+    }
+    return v;
+}
+
+// In-place inclusive max-scan of s[0..len) (each thread: `per` consecutive).
+__device__ __forceinline__ void block_incl_maxscan(uint32_t *s, int len, uint32_t *tmp) {
+    const int per = (len + blockDim.x - 1) / blockDim.x;
+    const int beg = threadIdx.x * per;
+    uint32_t local = 0;
+    for (int i = 0; i < per; i++)
+        if (beg + i < len) local = s[beg + i] > local ? s[beg + i] : local;
+    const uint32_t incl = warp_incl_max(local);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if (lane == 31) tmp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = lane < nw ? tmp[lane] : 0;
+        uint32_t vi = warp_incl_max(v);
+        uint32_t ex = __shfl_up_sync(0xffffffffu, vi, 1);
+        if (lane < nw) tmp[lane] = lane ? ex : 0;
+    }
+    __syncthreads();
+    uint32_t run = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) run = 0;
+    run = run > tmp[w] ? run : tmp[w];
+    for (int i = 0; i < per; i++) {
+        if (beg + i < len) {
+            run = s[beg + i] > run ? s[beg + i] : run;
+            s[beg + i] = run;
+        }
+    }
+    __syncthreads();
 }
 
 }  // namespace ls

@@ -25,6 +25,7 @@ void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st);
 
 // in-bucket sort (ls_sortsub.cu)
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);
+void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);
 void launch_big(const Args &a, int level, int dtype, cudaStream_t st);
 
 // parity hooks (ls_partition.cu)

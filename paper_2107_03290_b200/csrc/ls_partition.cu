@@ -25,6 +25,7 @@ __global__ void k_init(Ctl *ctl) {
     if (threadIdx.x == 0) {
         ctl->status = 0;
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
+        ctl->nchunks = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
         ctl->smin = ~0ull;
         ctl->smax = 0;
@@ -293,8 +294,16 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
             atomicMax(&a.tile_last[t], (uint32_t)g);
         } else {
             const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
-            if (k < a.big_cap) a.big[k] = BigItem{st, c, 0u, (uint32_t)g};
-            else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+            if (k < a.big_cap) {
+                a.big[k] = BigItem{st, c, 0u, (uint32_t)g, ~0ull, 0ull, 0u, 0u};
+                const uint32_t nch = (c + MM_CHUNK - 1) / MM_CHUNK;
+                const uint32_t base = atomicAdd(&a.ctl->nchunks, nch);
+                for (uint32_t q = 0; q < nch; q++)
+                    if (base + q < a.chunk_cap) a.chunks[base + q] = BigChunk{k, q};
+                    else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+            } else {
+                atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+            }
         }
     }
 }

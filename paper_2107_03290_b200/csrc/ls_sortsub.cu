@@ -5,9 +5,8 @@
 // running totals, placement (R4) -- followed by the touch-up. Because p is
 // monotone (R15) the only disorder left after the counting sort is inside runs
 // of equal pos ("collision groups"), so the global insertion sort of P:219 is
-// replaced by sorting every collision group independently: the paper's
-// insertion sort by one lane for groups <= 16 keys, a warp bitonic network for
-// larger ones. Homogeneous sub-buckets (min == max) are skipped.
+// replaced by ordering every collision group independently (rank within the
+// group). Homogeneous sub-buckets (min == max) are skipped.
 //
 // BIG sub-buckets (n' > T_small, north_star (3) "high-multiplicity"): the model
 // cannot separate their keys, so they take an exact path: MSD
@@ -70,129 +69,179 @@ __device__ __forceinline__ void bitonic(uint64_t *g, int c, int lane, int lanes)
 }
 
 // ----------------------------------------------------------- SMALL path ----
-// One CTA per window of T_tile key positions; it owns every SMALL sub-bucket
+// One CTA per window of T_tile key positions. It owns every SMALL sub-bucket
 // that starts in the window (classify recorded the first/last one), so its
-// span is at most T_tile + T_small keys. One warp per sub-bucket.
+// span [lo, hi) holds at most T_tile + T_small keys; the span is staged into
+// shared memory by the TMA bulk engine. All sub-buckets of the span are
+// processed at once, one thread per key:
+//   slot(key) = start(sub-bucket) + pos   for keys of SMALL sub-buckets
+//   slot(key) = own position              for everything else in the span
+// so one exclusive scan over the span's slots yields the counting-sort
+// placement of every sub-bucket at once (each sub-bucket's slots stay inside
+// its own range, so other keys keep their places). The touch-up then gives
+// every key its rank inside its collision group (run of equal slot) and
+// stores it at its final position: the insertion sort's result without its
+// divergent serial shifting. All-equal groups and homogeneous sub-buckets are
+// detected and skipped.
+constexpr int BS_THREADS = 512;
+constexpr int BS_KPT = 8;          // keys per thread; span cap = 4096
+constexpr int BS_SPAN = BS_THREADS * BS_KPT;
+
+struct BsSmem {
+    union {                        // the staged span lives in registers once the
+        uint64_t keys[BS_SPAN + 2];  // slots are known, so the counting-sort target
+        uint64_t T[BS_SPAN + 2];     // T reuses its storage
+    };
+    uint32_t K[BS_SPAN + 1];       // slot histogram -> exclusive scan
+    uint32_t seg[BS_SPAN];         // local sub-bucket id of each position (max-scan)
+    uint32_t gnp[BS_SPAN];         // at a sub-bucket's head: g | n' << 20
+    uint8_t diff[BS_SPAN];         // at a sub-bucket's head: keys not all equal
+    uint8_t eq[BS_SPAN + 1];       // per slot: collision group is all-equal
+    uint32_t tmp[36];
+    unsigned long long st_small, st_smallk, st_h1, st_h1k, st_maxg;
+    uint64_t mbar;
+};
+
 template <int DT>
-__global__ void __launch_bounds__(256) k_bucketsort(Args a) {
+__global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
     if (a.ctl->status) return;
-    const uint32_t t = blockIdx.x;
-    const uint32_t g0 = a.tile_first[t];
+    const uint4 desc = a.tdesc[blockIdx.x];  // {g0, g1, lo, hi} (k_tile_desc)
+    const uint32_t g0 = desc.x, g1 = desc.y, lo = desc.z, hi = desc.w;
     if (g0 == 0xffffffffu) return;
-    const uint32_t g1 = a.tile_last[t];
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int span_cap = a.T_tile + a.T_small;
-    uint64_t *skeys = (uint64_t *)smem_raw;
-    uint64_t *stmp = skeys + span_cap;
-    uint32_t *sK = (uint32_t *)(stmp + span_cap);
-    uint32_t *spr = sK + span_cap;
-    __shared__ unsigned long long s_stat[5];
-    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = bd >> 5;
-    if (tid < 5) s_stat[tid] = 0;
-    const uint32_t lo = a.start1[g0];
-    const uint32_t hi = a.start1[g1] + a.hist1[g1];
-    for (uint32_t i = tid; i < hi - lo; i += bd) skeys[i] = a.A[lo + i];
-    __syncthreads();
-    const Root R = load_root(a.M);
-    const int f = a.f;
-    unsigned long long st_small = 0, st_smallk = 0, st_h1 = 0, st_h1k = 0, st_maxg = 0;
-    for (uint32_t g = g0 + warp; g <= g1; g += nwarps) {
-        const uint32_t np = a.hist1[g];
-        if (np < 2 || np > a.T_small) continue;
-        const uint32_t s = a.start1[g];
-        const uint32_t off = s - lo;
-        uint64_t *K = skeys + off;
-        uint64_t *T = stmp + off;
-        uint32_t *cK = sK + off;
-        uint32_t *pr = spr + off;
-        // Is-Homogeneous
-        unsigned long long mn = ~0ull, mx = 0;
-        for (uint32_t k = lane; k < np; k += 32) {
-            const unsigned long long o = to_ord<DT>(K[k]);
-            mn = o < mn ? o : mn;
-            mx = o > mx ? o : mx;
-        }
-        mn = warp_min_u64(mn);
-        mx = warp_max_u64(mx);
-        if (mn == mx) {
-            if (lane == 0) {
-                if (a.dH1) a.dH1[g] = 1;
-                st_h1++;
-                st_h1k += np;
-            }
-            continue;
-        }
-        // Model-based counting sort
-        for (uint32_t k = lane; k < np; k += 32) cK[k] = 0;
-        __syncwarp();
-        const double adj = __ddiv_rn((double)g, a.F2);  // (i*f + j)/f^2
-        const double top = (double)(np - 1);
-        for (uint32_t k = lane; k < np; k += 32) {
-            const double p = predict_ldg<DT>(K[k], R, a.M->leaf);
-            const uint32_t pos = cs_pos(p, adj, a.nd, top);
-            const uint32_t r = atomicAdd(&cK[pos], 1u);
-            pr[k] = pos | (r << 16);
-        }
-        __syncwarp();
-        uint32_t carry = 0;  // running totals, exclusive form (R4)
-        for (uint32_t base = 0; base < np; base += 32) {
-            const uint32_t k = base + lane;
-            const uint32_t v = k < np ? cK[k] : 0;
-            const uint32_t incl = warp_incl_scan(v);
-            if (k < np) cK[k] = carry + incl - v;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        __syncwarp();
-        for (uint32_t k = lane; k < np; k += 32) {  // placement
-            const uint32_t q = pr[k];
-            T[cK[q & 0xffffu] + (q >> 16)] = K[k];
-        }
-        __syncwarp();
-        // Touch-up per collision group (R15)
-        uint32_t maxg = 0;
-        for (uint32_t base = 0; base < np; base += 32) {
-            const uint32_t k = base + lane;
-            uint32_t c = 0, st = 0;
-            if (k < np) {
-                st = cK[k];
-                c = (k + 1 < np ? cK[k + 1] : np) - st;
-            }
-            maxg = c > maxg ? c : maxg;
-            if (c >= 2 && c <= 16) insertion_sort<DT>(T + st, (int)c);
-            unsigned big = __ballot_sync(0xffffffffu, c > 16);
-            while (big) {
-                const int leader = __ffs(big) - 1;
-                const uint32_t bst = __shfl_sync(0xffffffffu, st, leader);
-                const uint32_t bc = __shfl_sync(0xffffffffu, c, leader);
-                bitonic<DT, false>(T + bst, (int)bc, lane, 32);
-                big &= big - 1;
-            }
-            __syncwarp();
-        }
-        for (uint32_t k = lane; k < np; k += 32) a.A[s + k] = T[k];
-        maxg = (uint32_t)warp_max_u64(maxg);
-        if (lane == 0) {
-            st_small++;
-            st_smallk += np;
-            st_maxg = maxg > st_maxg ? maxg : st_maxg;
+    BsSmem &S = *reinterpret_cast<BsSmem *>(smem_raw);
+    const int tid = threadIdx.x, bd = blockDim.x;
+    const int span = (int)(hi - lo);
+    // zero the per-span tables while the bulk copy is in flight
+    if (tid == 0) {
+        S.st_small = S.st_smallk = S.st_h1 = S.st_h1k = S.st_maxg = 0;
+    }
+    for (int i = tid; i <= span; i += bd) S.K[i] = 0;
+    for (int i = tid; i < span; i += bd) {
+        S.seg[i] = 0;
+        S.diff[i] = 0;
+    }
+    const uint64_t *keys = stage_keys(a.A, lo, hi, S.keys, &S.mbar);
+    // sub-bucket heads (P:176-183 iterate the sub-buckets of the window)
+    for (uint32_t g = g0 + tid; g <= g1; g += bd) {
+        const uint32_t np = __ldg(&a.hist1[g]);
+        if (np >= 1) {
+            const uint32_t h = __ldg(&a.start1[g]) - lo;
+            S.seg[h] = h + 1;  // max-scan -> head position + 1 of the covering sub-bucket
+            S.gnp[h] = g | (np << 20);  // f*f <= 2^20, n' <= 2048
         }
     }
-    if (lane == 0) {
-        if (st_small) atomicAdd(&s_stat[0], st_small);
-        if (st_smallk) atomicAdd(&s_stat[1], st_smallk);
-        if (st_h1) atomicAdd(&s_stat[2], st_h1);
-        if (st_h1k) atomicAdd(&s_stat[3], st_h1k);
-        if (st_maxg) atomicMax(&s_stat[4], st_maxg);
+    __syncthreads();
+    block_incl_maxscan(S.seg, span, S.tmp);
+    // counting-sort slots (Alg. 2)
+    const Root R = load_root(a.M);
+    uint32_t packed[BS_KPT];
+    uint64_t kv[BS_KPT];
+#pragma unroll
+    for (int j = 0; j < BS_KPT; j++) {
+        const int i = j * bd + tid;
+        packed[j] = 0xffffffffu;
+        if (i < span) {
+            const uint32_t st = S.seg[i] - 1;
+            const uint32_t gnp = S.gnp[st];
+            const uint32_t g = gnp & 0xfffffu, np = gnp >> 20;
+            const uint64_t key = keys[i];
+            kv[j] = key;
+            uint32_t slot = (uint32_t)i;
+            if ((uint32_t)i - st < np && np >= 2) {
+                const double p = predict_ldg<DT>(key, R, a.M->leaf);
+                const double adj = __ddiv_rn((double)g, a.F2);  // (i*f + j)/f^2
+                slot = st + cs_pos(p, adj, a.nd, (double)(np - 1));
+                if (key != keys[st]) S.diff[st] = 1;
+            }
+            const uint32_t r = atomicAdd(&S.K[slot], 1u);
+            packed[j] = slot | (r << 16);
+        }
+    }
+    __syncthreads();
+    block_exscan(S.K, span + 1, S.tmp);  // running totals, exclusive (R4)
+#pragma unroll
+    for (int j = 0; j < BS_KPT; j++)  // placement
+        if (packed[j] != 0xffffffffu) S.T[S.K[packed[j] & 0xffffu] + (packed[j] >> 16)] = kv[j];
+    __syncthreads();
+    // all-equal collision groups need no ordering: every key compares itself
+    // with its group's first key (flag set by the rank-0 key, cleared on a mismatch)
+#pragma unroll
+    for (int j = 0; j < BS_KPT; j++) {
+        if (packed[j] == 0xffffffffu || (packed[j] >> 16) != 0) continue;
+        const uint32_t slot = packed[j] & 0xffffu;
+        S.eq[slot] = 1;
+        const uint32_t c = S.K[slot + 1] - S.K[slot];
+        if (c > 1 && S.diff[S.seg[j * bd + tid] - 1]) atomicMax(&S.st_maxg, (unsigned long long)c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < BS_KPT; j++) {
+        if (packed[j] == 0xffffffffu) continue;
+        const uint32_t slot = packed[j] & 0xffffu;
+        if (S.T[S.K[slot]] != kv[j]) S.eq[slot] = 0;
+    }
+    __syncthreads();
+    // Touch-up per collision group (R15): every key computes its rank
+    // inside its group (keys strictly before it + equal keys placed before it)
+    // and is stored at its final position -- the insertion sort's result,
+    // without its serial shifting. Sub-buckets that are not homogeneous are
+    // written back; the rest of the span is untouched.
+#pragma unroll
+    for (int j = 0; j < BS_KPT; j++) {
+        const int i = j * bd + tid;
+        if (packed[j] == 0xffffffffu) continue;
+        const uint32_t st = S.seg[i] - 1;  // head position of this key's sub-bucket
+        if (!S.diff[st]) continue;        // homogeneous or not counting-sorted
+        const uint32_t slot = packed[j] & 0xffffu, r = packed[j] >> 16;
+        const uint32_t base = S.K[slot], c = S.K[slot + 1] - base;
+        uint32_t fin = base + r;
+        if (c > 1 && !S.eq[slot]) {
+            const uint64_t o = to_ord<DT>(kv[j]);
+            uint32_t rank = 0;
+            for (uint32_t q = 0; q < c; q++) {
+                const uint64_t oq = to_ord<DT>(S.T[base + q]);
+                rank += (oq < o) || (oq == o && q < r);
+            }
+            fin = base + rank;
+        }
+        a.A[lo + fin] = kv[j];
+    }
+    // per sub-bucket classification: H1 or counting-sorted
+    for (uint32_t g = g0 + tid; g <= g1; g += bd) {
+        const uint32_t np = __ldg(&a.hist1[g]);
+        if (np < 2) continue;
+        if (S.diff[__ldg(&a.start1[g]) - lo]) {
+            atomicAdd(&S.st_small, 1ull);
+            atomicAdd(&S.st_smallk, (unsigned long long)np);
+        } else {
+            if (a.dH1) a.dH1[g] = 1;
+            atomicAdd(&S.st_h1, 1ull);
+            atomicAdd(&S.st_h1k, (unsigned long long)np);
+        }
     }
     __syncthreads();
     if (tid == 0) {
-        if (s_stat[0]) atomicAdd(&a.ctl->stat[ST_SMALLS], s_stat[0]);
-        if (s_stat[1]) atomicAdd(&a.ctl->stat[ST_SMALLK], s_stat[1]);
-        if (s_stat[2]) atomicAdd(&a.ctl->stat[ST_H1S], s_stat[2]);
-        if (s_stat[3]) atomicAdd(&a.ctl->stat[ST_H1K], s_stat[3]);
-        if (s_stat[4]) atomicMax(&a.ctl->stat[ST_MAXGRP], s_stat[4]);
+        if (S.st_small) atomicAdd(&a.ctl->stat[ST_SMALLS], S.st_small);
+        if (S.st_smallk) atomicAdd(&a.ctl->stat[ST_SMALLK], S.st_smallk);
+        if (S.st_h1) atomicAdd(&a.ctl->stat[ST_H1S], S.st_h1);
+        if (S.st_h1k) atomicAdd(&a.ctl->stat[ST_H1K], S.st_h1k);
+        if (S.st_maxg) atomicMax(&a.ctl->stat[ST_MAXGRP], S.st_maxg);
     }
+}
+
+// {g0, g1, lo, hi} per bucket-sort window: one dependent load per CTA instead
+// of two chained ones on the critical path of every tile.
+__global__ void k_tile_desc(Args a) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.ntiles) return;
+    const uint32_t g0 = a.tile_first[t];
+    uint4 d = make_uint4(0xffffffffu, 0u, 0u, 0u);
+    if (g0 != 0xffffffffu) {
+        const uint32_t g1 = a.tile_last[t];
+        d = make_uint4(g0, g1, a.start1[g0], a.start1[g1] + a.hist1[g1]);
+    }
+    a.tdesc[t] = d;
 }
 
 // ------------------------------------------------------------- BIG path ----
@@ -200,16 +249,70 @@ constexpr int BIG_THREADS = 512;
 constexpr int BIG_DIGITS = 4096;       // 12-bit MSD digits
 constexpr int BIG_SORT_CAP = 8192;     // keys sorted in shared memory by one CTA
 constexpr int BIG_CHUNK = BIG_SORT_CAP / 2;
+constexpr int BIG_MAXWIN = 1024;       // windows classified per round
+constexpr int BIG_MAXBLK = 64;         // pieces in (BIG_CHUNK, BIG_SORT_CAP] per item
+
+// ord min/max of level-0 big items, one 64K-key chunk per work entry
+// (classify wrote the chunk list), so a multi-million-key homogeneous
+// sub-bucket (Zipf's top value, config 4's top level) is scanned by the whole
+// GPU instead of one CTA.
+template <int DT>
+__global__ void __launch_bounds__(512) k_big_minmax(Args a) {
+    if (a.ctl->status) return;
+    __shared__ unsigned long long red[64];
+    const uint32_t nch = min(a.ctl->nchunks, a.chunk_cap);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t e = blockIdx.x; e < nch; e += gridDim.x) {
+        const BigChunk ch = a.chunks[e];
+        const BigItem item = a.big[ch.item];
+        const uint32_t beg = ch.chunk * MM_CHUNK, end = min(item.size, beg + MM_CHUNK);
+        const uint64_t *X = a.A + item.off;
+        unsigned long long mn = ~0ull, mx = 0;
+        for (uint32_t i = beg + threadIdx.x; i < end; i += 4 * blockDim.x) {
+            uint64_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = (i + q * blockDim.x < end) ? X[i + q * blockDim.x] : X[beg];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const unsigned long long o = to_ord<DT>(v[q]);
+                mn = o < mn ? o : mn;
+                mx = o > mx ? o : mx;
+            }
+        }
+        mn = warp_min_u64(mn);
+        mx = warp_max_u64(mx);
+        if ((threadIdx.x & 31) == 0) {
+            red[w] = mn;
+            red[32 + w] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < nw; k++) {
+                mn = red[k] < mn ? red[k] : mn;
+                mx = red[32 + k] > mx ? red[32 + k] : mx;
+            }
+            atomicMin(&a.big[ch.item].mn, mn);
+            atomicMax(&a.big[ch.item].mx, mx);
+        }
+        __syncthreads();
+    }
+}
 
 template <int DT>
 __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long &mn,
                            unsigned long long &mx, unsigned long long *red) {
     mn = ~0ull;
     mx = 0;
-    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) {
-        const unsigned long long o = to_ord<DT>(X[i]);
-        mn = o < mn ? o : mn;
-        mx = o > mx ? o : mx;
+    for (uint32_t i = threadIdx.x; i < size; i += 4 * blockDim.x) {
+        uint64_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = (i + q * blockDim.x < size) ? X[i + q * blockDim.x] : X[0];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const unsigned long long o = to_ord<DT>(v[q]);
+            mn = o < mn ? o : mn;
+            mx = o > mx ? o : mx;
+        }
     }
     mn = warp_min_u64(mn);
     mx = warp_max_u64(mx);
@@ -228,33 +331,50 @@ __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long 
     __syncthreads();
 }
 
+struct BigSmem {
+    uint64_t sk[BIG_SORT_CAP];
+    uint32_t start[BIG_DIGITS], end[BIG_DIGITS];
+    uint32_t wlo[BIG_MAXWIN], whi[BIG_MAXWIN];
+    uint32_t blk[BIG_MAXBLK];
+    uint32_t tmp[36];
+    uint32_t item, nblk;
+    unsigned long long red[64];
+};
+
+// One CTA per big item of this level: MSD radix partition X -> Y on the top
+// 12 bits of ord - min, then every piece is sorted exactly in shared memory
+// and written to A. Pieces <= BIG_CHUNK are gathered in windows of
+// BIG_CHUNK positions (a window owns the pieces starting in it, so its span
+// is <= BIG_SORT_CAP): one thread per piece of <= 16 keys (insertion sort),
+// one warp per larger piece (bitonic). Pieces in (BIG_CHUNK, BIG_SORT_CAP]
+// are block-sorted; larger ones become items of the next level.
 template <int DT>
-__global__ void __launch_bounds__(BIG_THREADS) k_big(Args a, int level) {
+__global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
     if (a.ctl->status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t *sk = (uint64_t *)smem_raw;                 // [BIG_SORT_CAP]
-    uint32_t *hist = (uint32_t *)(sk + BIG_SORT_CAP);    // [BIG_DIGITS]
-    uint32_t *cur = hist + BIG_DIGITS;                   // [BIG_DIGITS]
-    __shared__ unsigned long long red[64];
-    __shared__ uint32_t tmp[33];
-    __shared__ uint32_t s_item, s_dlo, s_dhi;
+    BigSmem &S = *reinterpret_cast<BigSmem *>(smem_raw);
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
     const uint32_t cnt = min(a.ctl->big_cnt[level], a.big_cap);
     const BigItem *list = a.big + (size_t)level * a.big_cap;
     for (;;) {
-        if (tid == 0) s_item = atomicAdd(&a.ctl->big_next[level], 1u);
+        if (tid == 0) S.item = atomicAdd(&a.ctl->big_next[level], 1u);
         __syncthreads();
-        const uint32_t it = s_item;
+        const uint32_t it = S.item;
         __syncthreads();
         if (it >= cnt) break;
         const BigItem item = list[it];
-        uint64_t *X = (item.in_b ? a.B : a.A) + item.off;
+        const uint64_t *X = (item.in_b ? a.B : a.A) + item.off;
         uint64_t *Y = (item.in_b ? a.A : a.B) + item.off;
         uint64_t *Aout = a.A + item.off;
         unsigned long long mn, mx;
-        big_minmax<DT>(X, item.size, mn, mx, red);
-        if (mn == mx) {  // homogeneous: already final
+        if (level == 0) {
+            mn = item.mn;
+            mx = item.mx;
+        } else {
+            big_minmax<DT>(X, item.size, mn, mx, S.red);
+        }
+        if (mn == mx) {  // homogeneous (P:183): already final
             if (item.in_b)
                 for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = X[i];
             if (tid == 0 && level == 0) {
@@ -262,6 +382,7 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big(Args a, int level) {
                 atomicAdd(&a.ctl->stat[ST_H1S], 1ull);
                 atomicAdd(&a.ctl->stat[ST_H1K], (unsigned long long)item.size);
             }
+            __syncthreads();
             continue;
         }
         if (tid == 0) {
@@ -272,10 +393,10 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big(Args a, int level) {
             atomicAdd(&a.ctl->stat[ST_BIGPASS], 1ull);
         }
         if (item.size <= BIG_SORT_CAP) {
-            for (uint32_t i = tid; i < item.size; i += bd) sk[i] = X[i];
+            for (uint32_t i = tid; i < item.size; i += bd) S.sk[i] = X[i];
             __syncthreads();
-            bitonic<DT, true>(sk, (int)item.size, tid, bd);
-            for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = sk[i];
+            bitonic<DT, true>(S.sk, (int)item.size, tid, bd);
+            for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = S.sk[i];
             __syncthreads();
             continue;
         }
@@ -283,87 +404,104 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big(Args a, int level) {
         const unsigned long long range = mx - mn;
         const int bits = 64 - __clzll((long long)range);
         const int shift = bits > 12 ? bits - 12 : 0;
-        for (int d = tid; d < BIG_DIGITS; d += bd) hist[d] = 0;
+        for (int d = tid; d < BIG_DIGITS; d += bd) S.start[d] = 0;
+        if (tid == 0) S.nblk = 0;
         __syncthreads();
-        for (uint32_t i = tid; i < item.size; i += bd)
-            atomicAdd(&hist[(uint32_t)((to_ord<DT>(X[i]) - mn) >> shift)], 1u);
-        __syncthreads();
-        for (int d = tid; d < BIG_DIGITS; d += bd) cur[d] = hist[d];
-        __syncthreads();
-        block_exscan(cur, BIG_DIGITS, tmp);  // cur = piece starts
-        // keep starts in `hist` after the scatter: hist[d] = start, sizes from neighbours
-        for (int d = tid; d < BIG_DIGITS; d += bd) {
-            const uint32_t c = hist[d];
-            hist[d] = cur[d];
-            (void)c;
+        for (uint32_t i = tid; i < item.size; i += 4 * bd) {
+            uint64_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = (i + q * bd < item.size) ? X[i + q * bd] : 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (i + q * bd < item.size)
+                    atomicAdd(&S.start[(uint32_t)((to_ord<DT>(v[q]) - mn) >> shift)], 1u);
         }
         __syncthreads();
-        for (uint32_t i = tid; i < item.size; i += bd) {
-            const uint64_t key = X[i];
-            const uint32_t d = (uint32_t)((to_ord<DT>(key) - mn) >> shift);
-            Y[atomicAdd(&cur[d], 1u)] = key;
-        }
+        block_exscan(S.start, BIG_DIGITS, S.tmp);
+        for (int d = tid; d < BIG_DIGITS; d += bd) S.end[d] = S.start[d];
         __syncthreads();
-        // now hist[d] = start of piece d, cur[d] = end of piece d
+        for (uint32_t i = tid; i < item.size; i += 4 * bd) {
+            uint64_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = (i + q * bd < item.size) ? X[i + q * bd] : 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (i + q * bd < item.size) {
+                    const uint32_t d = (uint32_t)((to_ord<DT>(v[q]) - mn) >> shift);
+                    Y[atomicAdd(&S.end[d], 1u)] = v[q];
+                }
+        }
+        __syncthreads();  // S.end[d] = end of piece d; Y holds the pieces
+        if (shift == 0) {  // every piece holds a single value: Y is sorted
+            if (Y != Aout)
+                for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = Y[i];
+            __syncthreads();
+            continue;
+        }
         const bool y_is_b = !item.in_b;
-        // (a) pieces larger than BIG_CHUNK: sort in shared memory or defer
-        for (int d = 0; d < BIG_DIGITS; d++) {
-            const uint32_t ps = hist[d], pc = cur[d] - hist[d];
-            if (pc <= BIG_CHUNK) continue;
-            if (pc <= BIG_SORT_CAP) {
-                for (uint32_t i = tid; i < pc; i += bd) sk[i] = Y[ps + i];
-                __syncthreads();
-                bitonic<DT, true>(sk, (int)pc, tid, bd);
-                for (uint32_t i = tid; i < pc; i += bd) Aout[ps + i] = sk[i];
-                __syncthreads();
-            } else if (tid == 0) {
-                if (level + 1 < BIG_LEVELS) {
-                    const uint32_t k = atomicAdd(&a.ctl->big_cnt[level + 1], 1u);
-                    if (k < a.big_cap)
-                        a.big[(size_t)(level + 1) * a.big_cap + k] =
-                            BigItem{item.off + ps, pc, y_is_b ? 1u : 0u, ~0u};
-                    else
-                        atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-                } else {
-                    atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-                }
-            }
-        }
-        // (b) pieces <= BIG_CHUNK, in windows of BIG_CHUNK positions: a window
-        // owns the pieces starting in it (span <= 2*BIG_CHUNK = BIG_SORT_CAP)
         const uint32_t nwin = (item.size + BIG_CHUNK - 1) / BIG_CHUNK;
-        for (uint32_t w = 0; w < nwin; w++) {
-            const uint32_t wlo = w * BIG_CHUNK, whi = wlo + BIG_CHUNK;
-            if (tid == 0) {
-                int dlo = BIG_DIGITS, dhi = -1;
-                for (int d = 0; d < BIG_DIGITS; d++) {  // short scan: monotone starts
-                    const uint32_t ps = hist[d], pc = cur[d] - ps;
-                    if (ps >= whi) break;
-                    if (ps < wlo || pc == 0 || pc > BIG_CHUNK) continue;
-                    if (d < dlo) dlo = d;
-                    dhi = d;
-                }
-                s_dlo = (uint32_t)dlo;
-                s_dhi = (uint32_t)dhi;
+        for (uint32_t wbase = 0; wbase < nwin; wbase += BIG_MAXWIN) {
+            for (int w = tid; w < BIG_MAXWIN; w += bd) {
+                S.wlo[w] = BIG_DIGITS;
+                S.whi[w] = 0;
             }
             __syncthreads();
-            const int dlo = (int)s_dlo, dhi = (int)s_dhi;
-            if (dhi >= dlo) {
-                const uint32_t slo = hist[dlo], shi = cur[dhi];
-                for (uint32_t i = tid; i < shi - slo; i += bd) sk[i] = Y[slo + i];
-                __syncthreads();
-                for (int d = dlo + tid; d <= dhi; d += bd) {  // tiny pieces: one lane each
-                    const uint32_t pc = cur[d] - hist[d];
-                    if (pc >= 2 && pc <= 16) insertion_sort<DT>(sk + (hist[d] - slo), (int)pc);
+            for (int d = tid; d < BIG_DIGITS; d += bd) {  // classify the pieces in parallel
+                const uint32_t ps = S.start[d], pc = S.end[d] - ps;
+                if (pc == 0) continue;
+                if (pc <= BIG_CHUNK) {
+                    const uint32_t w = ps / BIG_CHUNK;
+                    if (w >= wbase && w < wbase + BIG_MAXWIN) {
+                        atomicMin(&S.wlo[w - wbase], (uint32_t)d);
+                        atomicMax(&S.whi[w - wbase], (uint32_t)d);
+                    }
+                } else if (wbase == 0) {
+                    uint32_t k = BIG_MAXBLK;
+                    if (pc <= BIG_SORT_CAP) k = atomicAdd(&S.nblk, 1u);
+                    if (k < BIG_MAXBLK) {
+                        S.blk[k] = (uint32_t)d;
+                    } else if (level + 1 < BIG_LEVELS) {  // next level
+                        const uint32_t q = atomicAdd(&a.ctl->big_cnt[level + 1], 1u);
+                        if (q < a.big_cap)
+                            a.big[(size_t)(level + 1) * a.big_cap + q] =
+                                BigItem{item.off + ps, pc, y_is_b ? 1u : 0u, ~0u, ~0ull, 0ull, 0u, 0u};
+                        else
+                            atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+                    } else {
+                        atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+                    }
                 }
-                for (int d = dlo + warp; d <= dhi; d += nwarps) {  // larger: one warp each
-                    const uint32_t pc = cur[d] - hist[d];
-                    if (pc > 16 && pc <= BIG_CHUNK)
-                        bitonic<DT, false>(sk + (hist[d] - slo), (int)pc, lane, 32);
-                }
-                __syncthreads();
-                for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
             }
+            __syncthreads();
+            const uint32_t wend = min(nwin - wbase, (uint32_t)BIG_MAXWIN);
+            for (uint32_t w = 0; w < wend; w++) {
+                const uint32_t dlo = S.wlo[w], dhi = S.whi[w];
+                if (dlo > dhi) continue;  // uniform
+                const uint32_t slo = S.start[dlo], shi = S.end[dhi];
+                for (uint32_t i = tid; i < shi - slo; i += bd) S.sk[i] = Y[slo + i];
+                __syncthreads();
+                for (uint32_t d = dlo + tid; d <= dhi; d += bd) {  // one thread per tiny piece
+                    const uint32_t pc = S.end[d] - S.start[d];
+                    if (pc >= 2 && pc <= 16) insertion_sort<DT>(S.sk + (S.start[d] - slo), (int)pc);
+                }
+                for (uint32_t d = dlo + warp; d <= dhi; d += nwarps) {  // one warp per larger piece
+                    const uint32_t pc = S.end[d] - S.start[d];
+                    if (pc > 16 && pc <= BIG_CHUNK)
+                        bitonic<DT, false>(S.sk + (S.start[d] - slo), (int)pc, lane, 32);
+                }
+                __syncthreads();
+                for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = S.sk[i];
+                __syncthreads();
+            }
+        }
+        const uint32_t nblk = min(S.nblk, (uint32_t)BIG_MAXBLK);
+        for (uint32_t k = 0; k < nblk; k++) {
+            const uint32_t d = S.blk[k];
+            const uint32_t ps = S.start[d], pc = S.end[d] - ps;
+            for (uint32_t i = tid; i < pc; i += bd) S.sk[i] = Y[ps + i];
+            __syncthreads();
+            bitonic<DT, true>(S.sk, (int)pc, tid, bd);
+            for (uint32_t i = tid; i < pc; i += bd) Aout[ps + i] = S.sk[i];
             __syncthreads();
         }
     }
@@ -371,19 +509,24 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big(Args a, int level) {
 
 // -------------------------------------------------------------- launchers --
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
-    const size_t span = a.T_tile + a.T_small;
-    const size_t sm = span * (8 + 8 + 4 + 4);
+    k_tile_desc<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
+    const size_t sm = sizeof(BsSmem);
     if (dtype == DT_F64) {
         cudaFuncSetAttribute(k_bucketsort<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_bucketsort<DT_F64><<<a.ntiles, 256, sm, st>>>(a);
+        k_bucketsort<DT_F64><<<a.ntiles, BS_THREADS, sm, st>>>(a);
     } else {
         cudaFuncSetAttribute(k_bucketsort<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_bucketsort<DT_U64><<<a.ntiles, 256, sm, st>>>(a);
+        k_bucketsort<DT_U64><<<a.ntiles, BS_THREADS, sm, st>>>(a);
     }
 }
 
+void launch_big_minmax(const Args &a, int dtype, cudaStream_t st) {
+    if (dtype == DT_F64) k_big_minmax<DT_F64><<<148 * 4, 512, 0, st>>>(a);
+    else k_big_minmax<DT_U64><<<148 * 4, 512, 0, st>>>(a);
+}
+
 void launch_big(const Args &a, int level, int dtype, cudaStream_t st) {
-    const size_t sm = BIG_SORT_CAP * 8 + 2 * BIG_DIGITS * 4;
+    const size_t sm = sizeof(BigSmem);
     const int grid = 148 * 2;
     if (dtype == DT_F64) {
         cudaFuncSetAttribute(k_big<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
