@@ -2,6 +2,7 @@
 // sequence of Alg. 2 on one GPU, status/stats, and the parity hooks.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <memory>
@@ -258,6 +259,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     const Layout l = make_layout(n, cfg);
     if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
     Args a = make_args(l, d_keys, d_ws);
+    if (const char *e = getenv("LS_DEBUG_STAGE")) a.dbg = (uint32_t)atoi(e);
     const int dt = (int)dtype;
     unsigned char *w = (unsigned char *)d_ws;
     if (dumps) {

@@ -180,6 +180,7 @@ struct Args {
     uint32_t chunk_cap;
     // parity dumps (may be null)
     uint8_t *dH0, *dH1;
+    uint32_t dbg;  // LS_DEBUG_STAGE (profiling ablations only; 0 in normal use)
 };
 
 // ------------------------------------------------------------ scans -------

@@ -86,21 +86,35 @@ __device__ __forceinline__ void bitonic(uint64_t *g, int c, int lane, int lanes)
 constexpr int BS_THREADS = 512;
 constexpr int BS_KPT = 8;          // keys per thread; span cap = 4096
 constexpr int BS_SPAN = BS_THREADS * BS_KPT;
+constexpr int BS_WORDS = BS_SPAN / 32;
+constexpr int BS_MAXBIG = 128;     // collision groups > 8 keys per window
 
 struct BsSmem {
     union {                        // the staged span lives in registers once the
         uint64_t keys[BS_SPAN + 2];  // slots are known, so the counting-sort target
-        uint64_t T[BS_SPAN + 2];     // T reuses its storage
+        uint64_t T[BS_SPAN + 2];     // T (ord values) reuses its storage
     };
-    uint32_t K[BS_SPAN + 1];       // slot histogram -> exclusive scan
-    uint32_t seg[BS_SPAN];         // local sub-bucket id of each position (max-scan)
-    uint32_t gnp[BS_SPAN];         // at a sub-bucket's head: g | n' << 20
-    uint8_t diff[BS_SPAN];         // at a sub-bucket's head: keys not all equal
-    uint8_t eq[BS_SPAN + 1];       // per slot: collision group is all-equal
+    alignas(16) uint32_t K[BS_SPAN + 4];    // slot histogram -> exclusive scan
+    alignas(16) uint32_t gnp[BS_SPAN];      // at a head: g | n' << 20; after placement: slot of T[q]
+    alignas(16) uint32_t headbits[BS_WORDS];  // sub-bucket heads (bit per position)
+    alignas(16) uint32_t diffbits[BS_WORDS];  // at a head: the sub-bucket is not homogeneous
+    uint32_t wlast[BS_WORDS];               // 1 + last head position before word w (0: none)
+    uint32_t big[BS_MAXBIG];                // slots of collision groups > 8 keys
+    uint32_t nbig, ovf;
     uint32_t tmp[36];
     unsigned long long st_small, st_smallk, st_h1, st_h1k, st_maxg;
     uint64_t mbar;
 };
+
+// head position of the sub-bucket covering span position q
+__device__ __forceinline__ uint32_t head_of(const BsSmem &S, uint32_t q) {
+    const uint32_t w = q >> 5;
+    const uint32_t bits = S.headbits[w] & (0xffffffffu >> (31u - (q & 31u)));
+    return bits ? (w << 5) + 31u - __clz(bits) : S.wlast[w] - 1u;
+}
+__device__ __forceinline__ bool diff_at(const BsSmem &S, uint32_t h) {
+    return (S.diffbits[h >> 5] >> (h & 31u)) & 1u;
+}
 
 template <int DT>
 __global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
@@ -110,29 +124,59 @@ __global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
     if (g0 == 0xffffffffu) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BsSmem &S = *reinterpret_cast<BsSmem *>(smem_raw);
-    const int tid = threadIdx.x, bd = blockDim.x;
+    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int span = (int)(hi - lo);
-    // zero the per-span tables while the bulk copy is in flight
+    // stage the span with the TMA bulk engine; zero the tables meanwhile
+    const uint32_t alo = lo & ~1u, ahi = (hi + 1) & ~1u;
     if (tid == 0) {
+        mbar_init(&S.mbar, 1);
+        const uint32_t bytes = (ahi - alo) * 8u;
+        mbar_expect_tx(&S.mbar, bytes);
+        for (uint32_t o = 0; o < bytes; o += 16384)
+            bulk_g2s((char *)S.keys + o, (const char *)(a.A + alo) + o, bytes - o < 16384 ? bytes - o : 16384, &S.mbar);
+        S.nbig = S.ovf = 0;
         S.st_small = S.st_smallk = S.st_h1 = S.st_h1k = S.st_maxg = 0;
     }
-    for (int i = tid; i <= span; i += bd) S.K[i] = 0;
-    for (int i = tid; i < span; i += bd) {
-        S.seg[i] = 0;
-        S.diff[i] = 0;
+    {
+        uint4 *k4 = reinterpret_cast<uint4 *>(S.K);
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < (span + 4) / 4; i += bd) k4[i] = z;
+        if (tid < BS_WORDS) S.headbits[tid] = S.diffbits[tid] = 0;
     }
-    const uint64_t *keys = stage_keys(a.A, lo, hi, S.keys, &S.mbar);
+    __syncthreads();
     // sub-bucket heads (P:176-183 iterate the sub-buckets of the window)
     for (uint32_t g = g0 + tid; g <= g1; g += bd) {
         const uint32_t np = __ldg(&a.hist1[g]);
         if (np >= 1) {
             const uint32_t h = __ldg(&a.start1[g]) - lo;
-            S.seg[h] = h + 1;  // max-scan -> head position + 1 of the covering sub-bucket
+            atomicOr(&S.headbits[h >> 5], 1u << (h & 31u));
             S.gnp[h] = g | (np << 20);  // f*f <= 2^20, n' <= 2048
         }
     }
     __syncthreads();
-    block_incl_maxscan(S.seg, span, S.tmp);
+    if (warp == 0) {  // wlast: exclusive max-scan over the per-word last heads
+        uint32_t v[BS_WORDS / 32];
+        uint32_t run = 0;
+#pragma unroll
+        for (int k = 0; k < BS_WORDS / 32; k++) {
+            const int w = lane * (BS_WORDS / 32) + k;
+            const uint32_t b = S.headbits[w];
+            v[k] = b ? (uint32_t)(w << 5) + 32u - __clz(b) : 0u;  // last head + 1 in word w
+            run = v[k] > run ? v[k] : run;
+        }
+        uint32_t incl = warp_incl_max(run);
+        uint32_t ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) ex = 0;
+#pragma unroll
+        for (int k = 0; k < BS_WORDS / 32; k++) {
+            S.wlast[lane * (BS_WORDS / 32) + k] = ex;
+            ex = v[k] > ex ? v[k] : ex;
+        }
+    }
+    mbar_wait(&S.mbar, 0);
+    __syncthreads();
+    const uint64_t *keys = S.keys + (lo - alo);
+    if (a.dbg == 1) return;
     // counting-sort slots (Alg. 2)
     const Root R = load_root(a.M);
     uint32_t packed[BS_KPT];
@@ -142,7 +186,7 @@ __global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
         const int i = j * bd + tid;
         packed[j] = 0xffffffffu;
         if (i < span) {
-            const uint32_t st = S.seg[i] - 1;
+            const uint32_t st = head_of(S, (uint32_t)i);
             const uint32_t gnp = S.gnp[st];
             const uint32_t g = gnp & 0xfffffu, np = gnp >> 20;
             const uint64_t key = keys[i];
@@ -152,66 +196,103 @@ __global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
                 const double p = predict_ldg<DT>(key, R, a.M->leaf);
                 const double adj = __ddiv_rn((double)g, a.F2);  // (i*f + j)/f^2
                 slot = st + cs_pos(p, adj, a.nd, (double)(np - 1));
-                if (key != keys[st]) S.diff[st] = 1;
+                if (key != keys[st] && !diff_at(S, st)) atomicOr(&S.diffbits[st >> 5], 1u << (st & 31u));
             }
             const uint32_t r = atomicAdd(&S.K[slot], 1u);
             packed[j] = slot | (r << 16);
         }
     }
     __syncthreads();
+    if (a.dbg == 3) return;
     block_exscan(S.K, span + 1, S.tmp);  // running totals, exclusive (R4)
-#pragma unroll
-    for (int j = 0; j < BS_KPT; j++)  // placement
-        if (packed[j] != 0xffffffffu) S.T[S.K[packed[j] & 0xffffu] + (packed[j] >> 16)] = kv[j];
-    __syncthreads();
-    // all-equal collision groups need no ordering: every key compares itself
-    // with its group's first key (flag set by the rank-0 key, cleared on a mismatch)
-#pragma unroll
-    for (int j = 0; j < BS_KPT; j++) {
-        if (packed[j] == 0xffffffffu || (packed[j] >> 16) != 0) continue;
-        const uint32_t slot = packed[j] & 0xffffu;
-        S.eq[slot] = 1;
-        const uint32_t c = S.K[slot + 1] - S.K[slot];
-        if (c > 1 && S.diff[S.seg[j * bd + tid] - 1]) atomicMax(&S.st_maxg, (unsigned long long)c);
-    }
-    __syncthreads();
+    // placement. T holds ord values (plain integer compares in the
+    // touch-up); gnp[q] now remembers the slot of T position q.
 #pragma unroll
     for (int j = 0; j < BS_KPT; j++) {
         if (packed[j] == 0xffffffffu) continue;
         const uint32_t slot = packed[j] & 0xffffu;
-        if (S.T[S.K[slot]] != kv[j]) S.eq[slot] = 0;
+        const uint32_t q = S.K[slot] + (packed[j] >> 16);
+        S.T[q] = to_ord<DT>(kv[j]);
+        S.gnp[q] = slot;
     }
     __syncthreads();
-    // Touch-up per collision group (R15): every key computes its rank
-    // inside its group (keys strictly before it + equal keys placed before it)
-    // and is stored at its final position -- the insertion sort's result,
-    // without its serial shifting. Sub-buckets that are not homogeneous are
-    // written back; the rest of the span is untouched.
-#pragma unroll
-    for (int j = 0; j < BS_KPT; j++) {
-        const int i = j * bd + tid;
-        if (packed[j] == 0xffffffffu) continue;
-        const uint32_t st = S.seg[i] - 1;  // head position of this key's sub-bucket
-        if (!S.diff[st]) continue;        // homogeneous or not counting-sorted
-        const uint32_t slot = packed[j] & 0xffffu, r = packed[j] >> 16;
-        const uint32_t base = S.K[slot], c = S.K[slot + 1] - base;
-        uint32_t fin = base + r;
-        if (c > 1 && !S.eq[slot]) {
-            const uint64_t o = to_ord<DT>(kv[j]);
-            uint32_t rank = 0;
-            for (uint32_t q = 0; q < c; q++) {
-                const uint64_t oq = to_ord<DT>(S.T[base + q]);
-                rank += (oq < o) || (oq == o && q < r);
+    if (a.dbg == 4) return;
+    // Touch-up per collision group (R15), in T order: every key takes
+    // its rank inside its group (keys strictly below it + equal keys placed
+    // before it) and is stored at its final position -- the insertion sort's
+    // result without its serial shifting. Groups of > 8 keys (typically the
+    // clamped top slot of a sparse sub-bucket, R5) are ordered by a warp.
+    // Only sub-buckets that are not homogeneous are written back.
+    uint32_t maxg = 0;
+    for (int q = tid; q < span; q += bd) {
+        if (!diff_at(S, head_of(S, (uint32_t)q))) continue;  // homogeneous / not counting-sorted
+        const uint32_t slot = S.gnp[q], base = S.K[slot], c = S.K[slot + 1] - base;
+        const uint64_t o = S.T[q];
+        uint32_t fin = (uint32_t)q;
+        if (c > 1) {
+            if ((uint32_t)q == base && c > maxg) maxg = c;
+            if (c <= 8) {
+                uint32_t rank = 0;
+                for (uint32_t k = 0; k < c; k++) {
+                    const uint64_t ok = S.T[base + k];
+                    rank += (ok < o) || (ok == o && base + k < (uint32_t)q);
+                }
+                fin = base + rank;
+            } else {
+                if ((uint32_t)q == base) {
+                    const uint32_t k = atomicAdd(&S.nbig, 1u);
+                    if (k < BS_MAXBIG) S.big[k] = slot;
+                    else S.ovf = 1;
+                }
+                continue;
             }
-            fin = base + rank;
         }
-        a.A[lo + fin] = kv[j];
+        a.A[lo + fin] = from_ord<DT>(o);
     }
+    maxg = (uint32_t)warp_max_u64(maxg);
+    if (lane == 0 && maxg > 1) atomicMax(&S.st_maxg, (unsigned long long)maxg);
+    __syncthreads();
+    if (a.dbg == 5) return;
+    // groups of > 8 keys: one warp each; all-equal groups are stored as they are
+    const uint32_t nb = min(S.nbig, (uint32_t)BS_MAXBIG);
+    for (uint32_t k = warp; k < nb + (S.ovf ? (uint32_t)span : 0u); k += bd >> 5) {
+        uint32_t slot;
+        if (k < nb) {
+            slot = S.big[k];
+        } else {  // overflow: scan all slots (rare)
+            slot = k - nb;
+            const uint32_t c = S.K[slot + 1] - S.K[slot];
+            if (c <= 8 || !diff_at(S, head_of(S, S.K[slot]))) continue;
+            bool listed = false;
+            for (uint32_t q = 0; q < nb; q++) listed |= (S.big[q] == slot);
+            if (listed) continue;
+        }
+        const uint32_t base = S.K[slot], c = S.K[slot + 1] - base;
+        if (c <= 32) {  // register bitonic network across the warp (one key per lane)
+            uint64_t v = (uint32_t)lane < c ? S.T[base + lane] : ~0ull;
+#pragma unroll
+            for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, jj);
+                    const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+                    v = keep_min ? (w < v ? w : v) : (w > v ? w : v);
+                }
+            }
+            if ((uint32_t)lane < c) a.A[lo + base + lane] = from_ord<DT>(v);
+            continue;
+        }
+        bool same = true;
+        for (uint32_t q = lane; q < c; q += 32) same &= (S.T[base + q] == S.T[base]);
+        if (!__all_sync(0xffffffffu, same)) bitonic<DT_U64, false>(S.T + base, (int)c, lane, 32);
+        for (uint32_t q = lane; q < c; q += 32) a.A[lo + base + q] = from_ord<DT>(S.T[base + q]);
+    }
+    if (a.dbg == 6) return;
     // per sub-bucket classification: H1 or counting-sorted
     for (uint32_t g = g0 + tid; g <= g1; g += bd) {
         const uint32_t np = __ldg(&a.hist1[g]);
         if (np < 2) continue;
-        if (S.diff[__ldg(&a.start1[g]) - lo]) {
+        if (diff_at(S, __ldg(&a.start1[g]) - lo)) {
             atomicAdd(&S.st_small, 1ull);
             atomicAdd(&S.st_smallk, (unsigned long long)np);
         } else {
