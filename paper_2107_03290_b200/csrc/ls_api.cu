@@ -287,6 +287,8 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         launch_fit_params(l.m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, a.M, dt, st);
         launches += 3;
     }
+    launch_b0_table(a.M, l.L, l.f, dt, st);
+    launches++;
     tm.mark(LS_PHASE_FIT);
     launch_count0(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, st);

@@ -50,12 +50,27 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 }
 
 // -------------------------------------------------------------- model ------
+// b0 as a search (exact): b0 is a monotone step function of ord(x) (R15:
+// a >= 0, hi_l <= lo_{l+1}), so b0(x) = #{b >= 1 : thr_b <= ord(x)} with
+// thr_b = min{o : b0(o) >= b}. k_b0_thresholds finds the f-1 thresholds by
+// bisection with the very predict()/bucket0() of the full path, and a uniform
+// grid of B0_CELLS cells over [xmin, xmax] (cell(x) monotone in ord) records,
+// per cell, the range of thresholds that fall inside it: cell = off | cnt<<10
+// (cnt saturates at 63 = "search to the end"). A key then costs the root
+// arithmetic, one 2-byte and ~cnt 8-byte shared-memory loads instead of five
+// 8-byte leaf loads and the fp64 leaf line.
+constexpr int B0_CELLS = 16384;
 // Device copy of F_A. leaf[] holds (a, c, b, lo, hi) per leaf, 40 bytes.
 struct DevModel {
     double xmin, xmax, root_scale, last;  // last = (double)(L-1)
     uint32_t L, degenerate;
     uint64_t n_sample;
     double leaf[LS_MAX_LEAVES * 5];
+    // b0 search structure (k_b0_thresholds / k_b0_cells)
+    double cell_scale;                        // B0_CELLS / (xmax - xmin), 0 if degenerate
+    uint32_t nthr, pad_;                      // valid thresholds: thr[0 .. nthr)
+    unsigned long long thr[LS_MAX_FANOUT];    // thr[b-1] = min{o : b0(o) >= b}
+    alignas(16) uint16_t cell[B0_CELLS];
 };
 
 // Root parameters held in registers (uniform across the grid).
@@ -72,6 +87,14 @@ __device__ __forceinline__ Root load_root(const DevModel *M) {
     r.last = M->last;
     r.Lm1 = (int)M->L - 1;
     return r;
+}
+
+// Root routing of O6: xc = clamp(x, xmin, xmax), leaf = trunc((xc - xmin) * rs).
+template <int DT>
+__device__ __forceinline__ int root_leaf(uint64_t bits, const Root &R, double &xc) {
+    xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
+    const double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    return (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
 }
 
 // O6: p = F_A(x). `leaf` may point to shared or global memory.
@@ -102,11 +125,47 @@ __device__ __forceinline__ uint32_t bucket0(double p, double F, int f) {
     long long b = __double2ll_rz(__dmul_rn(p, F));
     return (uint32_t)(b < f - 1 ? b : f - 1);
 }
+
 __device__ __forceinline__ uint32_t bucket1(double p, double F2, int f, uint32_t parent) {
     long long b = __double2ll_rz(__dmul_rn(p, F2)) - (long long)parent * f;
     b = b < 0 ? 0 : b;
     return (uint32_t)(b > f - 1 ? f - 1 : b);
 }
+
+// Grid cell of a key for the b0 search (monotone in ord).
+template <int DT>
+__device__ __forceinline__ int b0_cell(uint64_t bits, double xmin, double xmax, double cs) {
+    const double xc = clampd(xd<DT>(bits), xmin, xmax);
+    const double r = __dmul_rn(__dsub_rn(xc, xmin), cs);
+    return (r < (double)(B0_CELLS - 1)) ? (int)__double2ll_rz(r) : B0_CELLS - 1;
+}
+
+// b0 of a key from the thresholds (thr, cell in shared memory); bit-identical
+// to bucket0(predict(x)) by construction (see B0_CELLS).
+struct B0Search {
+    double xmin, xmax, cs;
+    uint32_t nthr;
+    const unsigned long long *thr;
+    const uint16_t *cell;
+    template <int DT>
+    __device__ __forceinline__ uint32_t get(uint64_t bits) const {
+        const uint32_t e = cell[b0_cell<DT>(bits, xmin, xmax, cs)];
+        uint32_t lo = e & 1023u, n = e >> 10;
+        if (n == 63u) n = nthr - lo;
+        const unsigned long long o = to_ord<DT>(bits);
+        while (n > 0) {
+            const uint32_t half = n >> 1;
+            if (thr[lo + half] <= o) {
+                lo += half + 1;
+                n -= half + 1;
+            } else {
+                n = half;
+            }
+        }
+        return lo;
+    }
+};
+
 // Alg.2 P:188-190 (R5): pos = clamp(floor((p - adj) * n), 0, n'-1)
 __device__ __forceinline__ uint32_t cs_pos(double p, double adj, double nd, double top) {
     double v = floor(__dmul_rn(__dsub_rn(p, adj), nd));

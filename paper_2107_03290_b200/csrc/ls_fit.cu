@@ -160,6 +160,98 @@ __global__ void __launch_bounds__(1024) k_fit_params(uint64_t m, int L, const Ct
     }
 }
 
+// ------------------------------------------------------- b0 search tables ---
+// thr_b = min{o : b0(o) >= b} for b = 1..f-1 by bisection over the non-NaN ord
+// domain, evaluating b0 with the same predict()/bucket0() as every other
+// path; then per grid cell the range of thresholds inside its ord range.
+template <int DT>
+__device__ __forceinline__ uint32_t b0_at(unsigned long long o, const Root &R, const double *leaf,
+                                          double F, int f) {
+    return bucket0(predict_ldg<DT>(from_ord<DT>(o), R, leaf), F, f);
+}
+template <int DT>
+__device__ __forceinline__ void ord_domain(unsigned long long &omin, unsigned long long &omax) {
+    omin = DT == DT_F64 ? 0x000FFFFFFFFFFFFFull : 0ull;   // ord(-inf)
+    omax = DT == DT_F64 ? 0xFFF0000000000000ull : ~0ull;  // ord(+inf)
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_b0_thresholds(DevModel *M, int f) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const Root R = load_root(M);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const double range = __dsub_rn(M->xmax, M->xmin);
+        M->cell_scale = (M->degenerate || !(range > 0.0)) ? 0.0 : __ddiv_rn((double)B0_CELLS, range);
+    }
+    if (b >= f) return;
+    unsigned long long lo, hi;
+    ord_domain<DT>(lo, hi);
+    const double F = (double)f;
+    if (b0_at<DT>(hi, R, M->leaf, F, f) < (uint32_t)b) {
+        M->thr[b - 1] = ~0ull;  // never reached: not counted in nthr
+        return;
+    }
+    while (lo < hi) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        if (b0_at<DT>(mid, R, M->leaf, F, f) >= (uint32_t)b) hi = mid; else lo = mid + 1;
+    }
+    M->thr[b - 1] = lo;
+    atomicMax(&M->nthr, (uint32_t)b);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= B0_CELLS) return;
+    const double xmin = M->xmin, xmax = M->xmax, cs = M->cell_scale;
+    unsigned long long omin, omax;
+    ord_domain<DT>(omin, omax);
+    auto first_ge = [&](int target, bool &none) {
+        unsigned long long lo = omin, hi = omax;
+        none = b0_cell<DT>(from_ord<DT>(hi), xmin, xmax, cs) < target;
+        while (lo < hi) {
+            const unsigned long long mid = lo + (hi - lo) / 2;
+            if (b0_cell<DT>(from_ord<DT>(mid), xmin, xmax, cs) >= target) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    bool none0, none1;
+    const unsigned long long s = first_ge(c, none0);
+    const unsigned long long e = c + 1 < B0_CELLS ? first_ge(c + 1, none1) : (none1 = true, 0ull);
+    uint32_t entry = 0;
+    if (!none0 && (none1 || e > s)) {  // cell c owns ords [s, o_hi]
+        const unsigned long long o_hi = none1 ? omax : e - 1;
+        const uint32_t V = M->nthr;
+        uint32_t off = 0, end = 0;  // #thr < s, #thr <= o_hi
+        for (uint32_t lo = 0, n = V; n > 0;) {
+            const uint32_t h = n >> 1;
+            if (M->thr[lo + h] < s) { lo += h + 1; n -= h + 1; } else n = h;
+            off = lo;
+        }
+        for (uint32_t lo = 0, n = V; n > 0;) {
+            const uint32_t h = n >> 1;
+            if (M->thr[lo + h] <= o_hi) { lo += h + 1; n -= h + 1; } else n = h;
+            end = lo;
+        }
+        const uint32_t cnt = end - off;
+        entry = off | ((cnt < 63u ? cnt : 63u) << 10);
+    }
+    M->cell[c] = (uint16_t)entry;
+}
+
+void launch_b0_table(DevModel *M, int L, int f, int dtype, cudaStream_t st) {
+    (void)L;
+    cudaMemsetAsync(&M->nthr, 0, sizeof(uint32_t), st);
+    const int g = (f + 255) / 256;
+    if (dtype == DT_F64) {
+        k_b0_thresholds<DT_F64><<<g, 256, 0, st>>>(M, f);
+        k_b0_cells<DT_F64><<<B0_CELLS / 256, 256, 0, st>>>(M);
+    } else {
+        k_b0_thresholds<DT_U64><<<g, 256, 0, st>>>(M, f);
+        k_b0_cells<DT_U64><<<B0_CELLS / 256, 256, 0, st>>>(M);
+    }
+}
+
 static int grid_for(uint64_t m, int block) {
     uint64_t g = (m + block - 1) / block;
     if (g > 148 * 8) g = 148 * 8;

@@ -14,6 +14,9 @@ void launch_fit_hist(const uint64_t *S, uint64_t m, int L, Ctl *ctl, uint32_t *l
 void launch_fit_params(uint64_t m, int L, Ctl *ctl, const uint32_t *leaf_cnt,
                        const unsigned long long *leaf_min, DevModel *M, int dtype, cudaStream_t st);
 
+// b0 threshold table of the model (ls_fit.cu), after the model is final
+void launch_b0_table(DevModel *M, int L, int f, int dtype, cudaStream_t st);
+
 // partition rounds (ls_partition.cu)
 void launch_init(const Args &a, cudaStream_t st);
 void launch_count0(const Args &a, int dtype, cudaStream_t st);

@@ -17,6 +17,7 @@
 // directly from their min key.
 #include "ls_launch.h"
 #include "ls_tile.cuh"
+#include "ls_tilepart.cuh"
 
 namespace ls {
 
@@ -56,11 +57,31 @@ struct ModelBucket {
 };
 
 // --------------------------------------------------------------- round 0 ---
+// b0 search tables in shared memory (count0 / scatter0)
+struct alignas(16) B0Smem {
+    unsigned long long thr[LS_MAX_FANOUT];
+    uint16_t cell[B0_CELLS];
+};
+
+__device__ __forceinline__ B0Search load_b0_search(B0Smem &T, const DevModel *M) {
+    const uint32_t V = M->nthr;
+    for (uint32_t i = threadIdx.x; i < V; i += blockDim.x) T.thr[i] = M->thr[i];
+    const uint4 *src = reinterpret_cast<const uint4 *>(M->cell);
+    uint4 *dst = reinterpret_cast<uint4 *>(T.cell);
+    for (int i = threadIdx.x; i < B0_CELLS / 8; i += blockDim.x) dst[i] = src[i];
+    return B0Search{M->xmin, M->xmax, M->cell_scale, V, T.thr, T.cell};
+}
+
+struct Count0Smem {
+    B0Smem b0;
+    uint32_t hist[LS_MAX_FANOUT];
+};
+
 template <int DT>
-__global__ void __launch_bounds__(512) k_count0(Args a) {
+__global__ void __launch_bounds__(512, 2) k_count0(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *leaf = (double *)smem_raw;
-    uint32_t *hist = (uint32_t *)(leaf + 5 * a.L);
+    Count0Smem &S = *reinterpret_cast<Count0Smem *>(smem_raw);
+    uint32_t *hist = S.hist;
     __shared__ uint32_t s_unit;
     __shared__ int s_nan;
     const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
@@ -68,23 +89,33 @@ __global__ void __launch_bounds__(512) k_count0(Args a) {
         s_unit = atomicAdd(&a.ctl->ticket0, 1u);
         s_nan = 0;
     }
-    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
+    const B0Search bs = load_b0_search(S.b0, a.M);
     for (int b = tid; b < f; b += bd) hist[b] = 0;
     __syncthreads();
     const uint64_t u = s_unit;
-    const Root R = load_root(a.M);
     const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
     bool nan = false;
     auto one = [&](uint64_t b) {
         if (DT == DT_F64 && is_nan_bits(b)) nan = true;
-        const double p = predict<DT>(b, R, leaf);
-        atomicAdd(&hist[bucket0(p, a.F, f)], 1u);
+        atomicAdd(&hist[bs.get<DT>(b)], 1u);
     };
     if ((((uintptr_t)(a.A + beg)) & 15) == 0) {
+        // 4 independent 16-byte loads in flight per thread
         const ulonglong2 *A2 = (const ulonglong2 *)(a.A + beg);
         const uint64_t np = (end - beg) / 2;
-        for (uint64_t i = tid; i < np; i += bd) {
-            ulonglong2 v = A2[i];
+        uint64_t i = tid;
+        for (; i + 3 * bd < np; i += 4 * bd) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = __ldcs(A2 + i + q * bd);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                one(v[q].x);
+                one(v[q].y);
+            }
+        }
+        for (; i < np; i += bd) {
+            const ulonglong2 v = __ldcs(A2 + i);
             one(v.x);
             one(v.y);
         }
@@ -130,27 +161,34 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     }
 }
 
+// Level-0 bucket through the b0 search tables (shared memory).
 template <int DT>
-__global__ void __launch_bounds__(512) k_scatter0(Args a) {
+struct B0Bucket {
+    B0Search bs;
+    __device__ __forceinline__ uint32_t operator()(uint64_t key, uint64_t) const {
+        return bs.get<DT>(key);
+    }
+};
+
+struct Scatter0Smem {
+    TpSmem tp;
+    uint32_t base[LS_MAX_FANOUT];
+    B0Smem b0;
+};
+
+template <int DT>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
     if (a.ctl->status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int KPT = 8;
-    const int f = a.f, tid = threadIdx.x, bd = blockDim.x;
-    uint64_t *skeys = (uint64_t *)smem_raw;  // [KPT*bd]
-    double *leaf = (double *)(skeys + KPT * bd);
-    uint32_t *base = (uint32_t *)(leaf + 5 * a.L);
-    uint32_t *cnt = base + f;
-    uint32_t *tst = cnt + f;
-    uint32_t *tmp = tst + f;  // 33
-    uint16_t *sbin = (uint16_t *)(tmp + 36);
-    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
+    Scatter0Smem &S = *reinterpret_cast<Scatter0Smem *>(smem_raw);
+    const int f = a.f, tid = threadIdx.x;
     const uint64_t u = blockIdx.x;
-    for (int b = tid; b < f; b += bd) base[b] = (uint32_t)a.start0[b] + a.offs0[u * f + b];
-    __syncthreads();
-    const Root R = load_root(a.M);
+    const B0Bucket<DT> bf{load_b0_search(S.b0, a.M)};
+    if (tid < f) S.base[tid] = (uint32_t)a.start0[tid] + a.offs0[u * f + tid];
+    tp_init(S.tp);
     const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
-    const ModelBucket<DT, 0, true> bf{R, leaf, a.F, a.F2, f, 0u};
-    tile_scatter<KPT>(a.A, a.B, beg, end, base, cnt, tst, skeys, sbin, tmp, f, bf);
+    uint32_t phase = 0;
+    tile_partition(S.tp, a.A, a.B, beg, end, S.base, f, bf, phase);
 }
 
 // --------------------------------------------------------------- round 1 ---
@@ -213,24 +251,23 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     }
 }
 
+struct Scatter1Smem {
+    TpSmem tp;
+    uint32_t base[LS_MAX_FANOUT];
+    uint32_t ustart[LS_MAX_FANOUT + 1];
+};
+
 template <int DT>
-__global__ void __launch_bounds__(512) k_scatter1(Args a) {
+__global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int KPT = 8;
-    __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
-    const int f = a.f, tid = threadIdx.x, bd = blockDim.x;
+    Scatter1Smem &S = *reinterpret_cast<Scatter1Smem *>(smem_raw);
+    const int f = a.f, tid = threadIdx.x, bd = TP_THREADS;
     const uint32_t u = blockIdx.x;
     if (u >= a.ctl->U1 || a.ctl->status) return;
-    uint64_t *skeys = (uint64_t *)smem_raw;  // [KPT*bd]
-    uint32_t *base = (uint32_t *)(skeys + KPT * bd);
-    uint32_t *cnt = base + f;
-    uint32_t *tst = cnt + f;
-    uint32_t *tmp = tst + f;
-    uint16_t *sbin = (uint16_t *)(tmp + 36);
-    for (int b = tid; b <= f; b += bd) ustart[b] = a.unit1_start[b];
+    for (int b = tid; b <= f; b += bd) S.ustart[b] = a.unit1_start[b];
     __syncthreads();
-    const int b = find_bucket(ustart, f, u);
-    const uint32_t slice = u - ustart[b];
+    const int b = find_bucket(S.ustart, f, u);
+    const uint32_t slice = u - S.ustart[b];
     const uint64_t bbeg = a.start0[b], bend = a.start0[b + 1];
     const uint64_t beg = bbeg + (uint64_t)slice * a.C1;
     const uint64_t end = umin64(bend, beg + a.C1);
@@ -242,15 +279,16 @@ __global__ void __launch_bounds__(512) k_scatter1(Args a) {
         for (uint64_t i = beg + tid; i < end; i += bd) a.A[i] = v;
         return;
     }
+    // sub-bucket starts of bucket b (exclusive scan of its S'_B row) + this unit's offsets
+    uint32_t *tst = S.tp.ex;
     for (int j = tid; j < f; j += bd) tst[j] = a.hist1[(uint64_t)b * f + j];
     __syncthreads();
-    block_exscan(tst, f, tmp);
-    for (int j = tid; j < f; j += bd)
-        base[j] = (uint32_t)bbeg + tst[j] + a.offs1[(uint64_t)u * f + j];
-    __syncthreads();
-    const Root R = load_root(a.M);
-    const ModelBucket<DT, 1, false> bf{R, a.M->leaf, a.F, a.F2, f, (uint32_t)b};
-    tile_scatter<KPT>(a.B, a.A, beg, end, base, cnt, tst, skeys, sbin, tmp, f, bf);
+    block_exscan(tst, f, S.tp.wsum);
+    for (int j = tid; j < f; j += bd) S.base[j] = (uint32_t)bbeg + tst[j] + a.offs1[(uint64_t)u * f + j];
+    tp_init(S.tp);
+    const ModelBucket<DT, 1, false> bf{load_root(a.M), a.M->leaf, a.F, a.F2, f, (uint32_t)b};
+    uint32_t phase = 0;
+    tile_partition(S.tp, a.B, a.A, beg, end, S.base, f, bf, phase);
 }
 
 // ------------------------------------------------------------- classify ----
@@ -343,36 +381,30 @@ __global__ void k_bucket_pos(const uint64_t *__restrict__ keys, uint64_t n, int 
 }
 
 // -------------------------------------------------------------- launchers --
-static size_t smem_count0(const Args &a) { return 5 * a.L * sizeof(double) + a.f * 4; }
-static size_t smem_scatter0(const Args &a) {
-    return 8 * 512 * 8 + 5 * a.L * 8 + 3 * a.f * 4 + 36 * 4 + 8 * 512 * 2;
-}
-static size_t smem_scatter1(const Args &a) { return 8 * 512 * 8 + 3 * a.f * 4 + 36 * 4 + 8 * 512 * 2; }
-
 template <class K>
 static void set_smem(K k, size_t bytes) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 void launch_count0(const Args &a, int dtype, cudaStream_t st) {
-    size_t sm = smem_count0(a);
+    const size_t sm = sizeof(Count0Smem);
     if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<a.U0, 512, sm, st>>>(a); }
     else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<a.U0, 512, sm, st>>>(a); }
 }
 void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st) { k_plan0<<<1, 1024, 0, st>>>(a, dS_B); }
 void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
-    size_t sm = smem_scatter0(a);
-    if (dtype == DT_F64) { set_smem(k_scatter0<DT_F64>, sm); k_scatter0<DT_F64><<<a.U0, 512, sm, st>>>(a); }
-    else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<a.U0, 512, sm, st>>>(a); }
+    const size_t sm = sizeof(Scatter0Smem);
+    if (dtype == DT_F64) { set_smem(k_scatter0<DT_F64>, sm); k_scatter0<DT_F64><<<a.U0, TP_THREADS, sm, st>>>(a); }
+    else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<a.U0, TP_THREADS, sm, st>>>(a); }
 }
 void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     if (dtype == DT_F64) k_count1<DT_F64><<<a.U1max, 512, 0, st>>>(a);
     else k_count1<DT_U64><<<a.U1max, 512, 0, st>>>(a);
 }
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
-    size_t sm = smem_scatter1(a);
-    if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64>, sm); k_scatter1<DT_F64><<<a.U1max, 512, sm, st>>>(a); }
-    else { set_smem(k_scatter1<DT_U64>, sm); k_scatter1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
+    const size_t sm = sizeof(Scatter1Smem);
+    if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64>, sm); k_scatter1<DT_F64><<<a.U1max, TP_THREADS, sm, st>>>(a); }
+    else { set_smem(k_scatter1<DT_U64>, sm); k_scatter1<DT_U64><<<a.U1max, TP_THREADS, sm, st>>>(a); }
 }
 void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st) {
     (void)dS_B1;

@@ -305,3 +305,26 @@ def test_full_size_200m(dist):
     del sh, sg, oi
     gb0 = ls.ls_bucket_ids(t, gm, ws=ws, want=("hist0",))["hist0"].cpu().numpy()
     assert np.array_equal(gb0, d["S_B"].cpu().numpy())
+
+
+# ------------------------------------------------------------- multi-GPU ---
+
+def test_sort_multi_single_rank():
+    """ls_sort_multi with a one-rank NCCL communicator: split sample, splitters,
+    destination count/scatter, NCCL send/recv to self, local sort. (N > 1 host
+    logic: tests/test_multi_gloo.py; this box has one GPU.)"""
+    comm = ls.Comm(0, 1, ls.Comm.unique_id())
+    try:
+        for dist, n in (("cfg5mix", 2_000_000), ("twodups", 300_001)):
+            keys = gen(dist, n, 1000)
+            h = to_np(keys)
+            out = torch.empty(n + 1000, dtype=keys.dtype, device=DEV)
+            n_out, st = ls.ls_sort_multi(comm, keys, out)
+            assert n_out == n
+            assert np.array_equal(bits(to_np(out[:n_out])), bits(O.sort(h)[0]))
+        small = torch.empty(10, dtype=keys.dtype, device=DEV)
+        with pytest.raises(ls.LSError) as e:
+            ls.ls_sort_multi(comm, keys, small)
+        assert e.value.status == ls.LS_E_CAPACITY
+    finally:
+        comm.close()
