@@ -40,7 +40,7 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        lb1, offs1, hist1, start1, tfirst, tlast, tdesc, big, chunks, hist1_u64, B;
+        lb1, offs1, hist1, start1, tfirst, tlast, wlist, big, chunks, hist1_u64, B;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
@@ -92,7 +92,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.offs0 = take((size_t)l.U0 * l.f * 4);
     l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
-    l.tdesc = take((size_t)l.ntiles * 16);
+    l.wlist = take((size_t)l.ntiles * 16);
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
@@ -114,6 +114,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.F = (double)l.f;
     a.F2 = (double)l.f * (double)l.f;
     a.nd = (double)l.n;
+    a.rcpF2 = 1.0 / a.F2;
     a.C0 = l.C0;
     a.C1 = l.C1;
     a.U0 = l.U0;
@@ -140,7 +141,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.start1 = (uint32_t *)(w + l.start1);
     a.tile_first = (uint32_t *)(w + l.tfirst);
     a.tile_last = (uint32_t *)(w + l.tlast);
-    a.tdesc = (uint4 *)(w + l.tdesc);
+    a.wlist = (uint4 *)(w + l.wlist);
     a.big = (BigItem *)(w + l.big);
     a.chunks = (BigChunk *)(w + l.chunks);
     a.chunk_cap = l.chunk_cap;
@@ -152,7 +153,7 @@ static ls_status check_config(const ls_config &c) {
     if (c.leaf_count < 1 || c.leaf_count > LS_MAX_LEAVES) { set_error("leaf_count out of range [1, 1024]"); return LS_E_INVALID; }
     if (c.sample_stride < 1) { set_error("sample_stride must be >= 1"); return LS_E_INVALID; }
     if (c.fit != 0) { set_error("only the chord fit (0) is implemented"); return LS_E_INVALID; }
-    if (c.big_threshold < 64 || c.big_threshold > 2048) { set_error("big_threshold out of range [64, 2048]"); return LS_E_INVALID; }
+    if (c.big_threshold < 64 || c.big_threshold > 1024) { set_error("big_threshold out of range [64, 1024]"); return LS_E_INVALID; }
     return LS_OK;
 }
 
@@ -367,6 +368,11 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
         for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(pend->ev[i]);
     }
     if (pend->model_out && pend->model_host) from_dev_model(*pend->model_host, pend->dtype, *pend->model_out);
+    if (getenv("LS_DEBUG_STAGE")) {
+        fprintf(stderr, "prof:");
+        for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
+        fprintf(stderr, "\n");
+    }
     if (c.status & STATUS_NAN) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
     if (c.status & STATUS_INTERNAL) { set_error("internal invariant violated (corrupt partition state)"); return LS_E_INTERNAL; }
     return LS_OK;
@@ -386,7 +392,7 @@ void ls_config_default(ls_config *c) {
     c->leaf_count = 1000;
     c->sample_stride = 100; // P:328 1% sample (R9)
     c->fit = 0;
-    c->big_threshold = 2048;
+    c->big_threshold = 1024;
     c->flags = 0;
 }
 

@@ -186,8 +186,10 @@ struct Ctl {
     uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
     uint32_t nchunks;                  // k_big_minmax work entries
+    uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
+    unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
 };
 
 // Big-path work item: a key range that must be sorted exactly.
@@ -211,6 +213,7 @@ struct Args {
     int f;        // fanout
     int L;
     double F, F2, nd;
+    double rcpF2;      // RN(1/f^2) for adj_of
     uint32_t C0, C1;   // level-0 / level-1 unit sizes (keys)
     uint32_t U0, U1max;
     uint32_t T_small;  // big threshold
@@ -233,7 +236,7 @@ struct Args {
     uint32_t *hist1;                  // [f*f]
     uint32_t *start1;                 // [f*f]
     uint32_t *tile_first, *tile_last; // [ntiles]
-    uint4 *tdesc;                     // [ntiles] {g0, g1, lo, hi}
+    uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]
     uint32_t chunk_cap;

@@ -27,10 +27,12 @@ __global__ void k_init(Ctl *ctl) {
         ctl->status = 0;
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
+        ctl->nwin = ctl->wticket = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
         ctl->smin = ~0ull;
         ctl->smax = 0;
         for (int i = 0; i < ST_NUM; i++) ctl->stat[i] = 0;
+        for (int i = 0; i < 16; i++) ctl->prof[i] = 0;
     }
 }
 

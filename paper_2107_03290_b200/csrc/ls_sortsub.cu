@@ -69,41 +69,53 @@ __device__ __forceinline__ void bitonic(uint64_t *g, int c, int lane, int lanes)
 }
 
 // ----------------------------------------------------------- SMALL path ----
-// One CTA per window of T_tile key positions. It owns every SMALL sub-bucket
-// that starts in the window (classify recorded the first/last one), so its
-// span [lo, hi) holds at most T_tile + T_small keys; the span is staged into
-// shared memory by the TMA bulk engine. All sub-buckets of the span are
-// processed at once, one thread per key:
-//   slot(key) = start(sub-bucket) + pos   for keys of SMALL sub-buckets
-//   slot(key) = own position              for everything else in the span
-// so one exclusive scan over the span's slots yields the counting-sort
-// placement of every sub-bucket at once (each sub-bucket's slots stay inside
-// its own range, so other keys keep their places). The touch-up then gives
-// every key its rank inside its collision group (run of equal slot) and
-// stores it at its final position: the insertion sort's result without its
-// divergent serial shifting. All-equal groups and homogeneous sub-buckets are
-// detected and skipped.
-constexpr int BS_THREADS = 512;
-constexpr int BS_KPT = 8;          // keys per thread; span cap = 4096
-constexpr int BS_SPAN = BS_THREADS * BS_KPT;
-constexpr int BS_WORDS = BS_SPAN / 32;
-constexpr int BS_MAXBIG = 128;     // collision groups > 8 keys per window
+// Windows: classify assigns every SMALL sub-bucket (2 <= n' <= T_small) to the
+// window of T_tile positions its start falls in (T_tile <= T_small), so a
+// window's span [lo, hi) -- its first to its last SMALL sub-bucket -- holds at
+// most T_tile + T_small - 1 < BS_W keys and only SMALL or single-key
+// sub-buckets. k_window_list compacts the non-empty windows.
+//
+// k_bucketsort is persistent (one 1024-thread CTA per SM) and pulls windows
+// from a ticket counter; the next window is staged by the TMA bulk engine
+// while the current one is sorted. Per window, one thread per key:
+//   slot(key) = start(sub-bucket) + pos(key)   (Alg. 2, R5; adj is
+//               precomputed per sub-bucket)    for keys of SMALL sub-buckets,
+//   slot(key) = own position                   for single-key sub-buckets;
+// K[slot]++ (the rank r comes back from the atomic), one exclusive scan over
+// the span gives every sub-bucket's counting-sort placement at once (each
+// sub-bucket's slots stay in its own range), keys are placed at K[slot] + r
+// (R4). Touch-up (R15): only runs of equal slot
+// ("collision groups") can be out of order, so the owner thread of each key
+// computes its rank inside its group (groups of <= 8) and the key is written
+// to its final position in shared memory; larger groups are sorted by a warp
+// (register bitonic <= 32, shared-memory bitonic above; all-equal groups are
+// left alone). The sorted span is stored back coalesced, skipping homogeneous
+// and single-key sub-buckets, whose keys are already in place.
+constexpr int BS_THREADS = 256;
+constexpr int BS_KPT = 8;
+constexpr int BS_W = BS_THREADS * BS_KPT;  // span capacity (4096 keys)
+constexpr int BS_WORDS = BS_W / 32;
+constexpr int BS_LOG_W = 11;
+static_assert((1 << BS_LOG_W) == BS_W, "BS_LOG_W");
+constexpr int BS_CTAS_PER_SM = 4;
+constexpr int BS_MAXBIG = 256;             // collision groups > BS_RANKMAX keys per window
+constexpr uint32_t BS_RANKMAX = 8;         // groups up to this size: owner-thread ranks
+constexpr uint32_t BS_NONE = 0xffffffffu;
 
 struct BsSmem {
-    union {                        // the staged span lives in registers once the
-        uint64_t keys[BS_SPAN + 2];  // slots are known, so the counting-sort target
-        uint64_t T[BS_SPAN + 2];     // T (ord values) reuses its storage
-    };
-    alignas(16) uint32_t K[BS_SPAN + 4];    // slot histogram -> exclusive scan
-    alignas(16) uint32_t gnp[BS_SPAN];      // at a head: g | n' << 20; after placement: slot of T[q]
-    alignas(16) uint32_t headbits[BS_WORDS];  // sub-bucket heads (bit per position)
-    alignas(16) uint32_t diffbits[BS_WORDS];  // at a head: the sub-bucket is not homogeneous
+    uint64_t ring[2][BS_W + 2];             // staged spans; the current one becomes T
+    alignas(16) uint32_t K[BS_W + 4];       // slot histogram -> exclusive running totals
+    uint32_t gnp[BS_W];                     // at a head: g | (n' - 1) << 20
+    uint16_t slot_of[BS_W];                 // after placement: slot of T position q
+    uint32_t headbits[BS_WORDS];            // sub-bucket heads (bit per position)
     uint32_t wlast[BS_WORDS];               // 1 + last head position before word w (0: none)
+    uint32_t wbits[BS_WORDS];               // positions to store back (non-homogeneous SMALL sub-buckets)
     uint32_t big[BS_MAXBIG];                // slots of collision groups > 8 keys
+    uint32_t wsum[33];
     uint32_t nbig, ovf;
-    uint32_t tmp[36];
+    uint4 desc[2];                          // {g0, g1, lo, hi} of the window in each slot
     unsigned long long st_small, st_smallk, st_h1, st_h1k, st_maxg;
-    uint64_t mbar;
+    uint64_t mbar[2];
 };
 
 // head position of the sub-bucket covering span position q
@@ -112,194 +124,410 @@ __device__ __forceinline__ uint32_t head_of(const BsSmem &S, uint32_t q) {
     const uint32_t bits = S.headbits[w] & (0xffffffffu >> (31u - (q & 31u)));
     return bits ? (w << 5) + 31u - __clz(bits) : S.wlast[w] - 1u;
 }
-__device__ __forceinline__ bool diff_at(const BsSmem &S, uint32_t h) {
-    return (S.diffbits[h >> 5] >> (h & 31u)) & 1u;
+
+// Stage A[lo, hi) into ring slot `slot` (key k at slot[k - (lo & ~1)]); thread 0 only.
+__device__ __forceinline__ void bs_issue(BsSmem &S, int slot, const uint64_t *A, uint32_t lo,
+                                         uint32_t hi) {
+    uint64_t *dst = S.ring[slot];
+    const uint32_t a0 = lo & ~1u, ilo = (lo + 1) & ~1u, ihi = hi & ~1u;
+    if (lo & 1u) dst[lo - a0] = A[lo];
+    if ((hi & 1u) && hi - 1 >= ilo) dst[hi - 1 - a0] = A[hi - 1];
+    const uint32_t bytes = ihi > ilo ? (ihi - ilo) * 8u : 0u;
+    mbar_expect_tx(&S.mbar[slot], bytes);
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+        bulk_g2s((char *)(dst + (ilo - a0)) + o, (const char *)(A + ilo) + o,
+                 bytes - o < 32768u ? bytes - o : 32768u, &S.mbar[slot]);
+}
+
+// Stage window descriptor d into `slot` (thread 0); the end of the CTA's
+// window sequence is signalled with desc.x = ~0 and an empty transaction so
+// the wait completes.
+__device__ __forceinline__ void bs_stage(BsSmem &S, int slot, const Args &a, uint4 d) {
+    S.desc[slot] = d;
+    if (d.x != BS_NONE) bs_issue(S, slot, a.A, d.z, d.w);
+    else mbar_expect_tx(&S.mbar[slot], 0u);
+}
+// CTA c sorts windows c, c + G, c + 2G, ... (G = gridDim.x): no ticket on the
+// critical path, and the descriptor two windows ahead is loaded early.
+__device__ __forceinline__ uint4 bs_desc(const Args &a, uint32_t nwin, uint32_t it) {
+    const uint32_t w = blockIdx.x + it * gridDim.x;
+    return w < nwin ? a.wlist[w] : make_uint4(BS_NONE, 0u, 0u, 0u);
+}
+
+// adj = g / f^2 correctly rounded, as (double)g * rcp plus one fma correction
+// step (rcp = RN(1/f^2)); exhaustively equal to the IEEE quotient for every
+// f <= 1024 and g < f^2 (tests/test_adj_division.py).
+__device__ __forceinline__ double adj_of(uint32_t g, double F2, double rcp) {
+    const double gd = (double)g;
+    const double q0 = __dmul_rn(gd, rcp);
+    return __fma_rn(__fma_rn(-q0, F2, gd), rcp, q0);
+}
+
+// Ascending bitonic sort of 32 (one per lane) or 64 (two per lane, element
+// lane + 32 s in v[s]) ord values across a warp, in registers.
+__device__ __forceinline__ void warp_sort32(uint64_t &v, int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            const uint64_t w = __shfl_xor_sync(0xffffffffu, v, jj);
+            const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+            v = keep_min ? (w < v ? w : v) : (w > v ? w : v);
+        }
+    }
+}
+__device__ __forceinline__ void warp_sort64(uint64_t v[2], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj == 32) {  // partner in the other register of the same lane (kk == 64: ascending)
+                const uint64_t lo_ = v[0] < v[1] ? v[0] : v[1], hi_ = v[0] < v[1] ? v[1] : v[0];
+                v[0] = lo_;
+                v[1] = hi_;
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < 2; s2++) {
+                    const int i = lane + 32 * s2;
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
+                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
+                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
+                }
+            }
+        }
+    }
 }
 
 template <int DT>
-__global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
+__global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args a) {
     if (a.ctl->status) return;
-    const uint4 desc = a.tdesc[blockIdx.x];  // {g0, g1, lo, hi} (k_tile_desc)
-    const uint32_t g0 = desc.x, g1 = desc.y, lo = desc.z, hi = desc.w;
-    if (g0 == 0xffffffffu) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BsSmem &S = *reinterpret_cast<BsSmem *>(smem_raw);
-    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int span = (int)(hi - lo);
-    // stage the span with the TMA bulk engine; zero the tables meanwhile
-    const uint32_t alo = lo & ~1u, ahi = (hi + 1) & ~1u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t nwin = min(a.ctl->nwin, a.ntiles);
     if (tid == 0) {
-        mbar_init(&S.mbar, 1);
-        const uint32_t bytes = (ahi - alo) * 8u;
-        mbar_expect_tx(&S.mbar, bytes);
-        for (uint32_t o = 0; o < bytes; o += 16384)
-            bulk_g2s((char *)S.keys + o, (const char *)(a.A + alo) + o, bytes - o < 16384 ? bytes - o : 16384, &S.mbar);
-        S.nbig = S.ovf = 0;
+        mbar_init(&S.mbar[0], 1);
+        mbar_init(&S.mbar[1], 1);
         S.st_small = S.st_smallk = S.st_h1 = S.st_h1k = S.st_maxg = 0;
-    }
-    {
-        uint4 *k4 = reinterpret_cast<uint4 *>(S.K);
-        const uint4 z = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < (span + 4) / 4; i += bd) k4[i] = z;
-        if (tid < BS_WORDS) S.headbits[tid] = S.diffbits[tid] = 0;
+        bs_stage(S, 0, a, bs_desc(a, nwin, 0));
+        bs_stage(S, 1, a, bs_desc(a, nwin, 1));
     }
     __syncthreads();
-    // sub-bucket heads (P:176-183 iterate the sub-buckets of the window)
-    for (uint32_t g = g0 + tid; g <= g1; g += bd) {
-        const uint32_t np = __ldg(&a.hist1[g]);
-        if (np >= 1) {
-            const uint32_t h = __ldg(&a.start1[g]) - lo;
-            atomicOr(&S.headbits[h >> 5], 1u << (h & 31u));
-            S.gnp[h] = g | (np << 20);  // f*f <= 2^20, n' <= 2048
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {  // wlast: exclusive max-scan over the per-word last heads
-        uint32_t v[BS_WORDS / 32];
-        uint32_t run = 0;
-#pragma unroll
-        for (int k = 0; k < BS_WORDS / 32; k++) {
-            const int w = lane * (BS_WORDS / 32) + k;
-            const uint32_t b = S.headbits[w];
-            v[k] = b ? (uint32_t)(w << 5) + 32u - __clz(b) : 0u;  // last head + 1 in word w
-            run = v[k] > run ? v[k] : run;
-        }
-        uint32_t incl = warp_incl_max(run);
-        uint32_t ex = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) ex = 0;
-#pragma unroll
-        for (int k = 0; k < BS_WORDS / 32; k++) {
-            S.wlast[lane * (BS_WORDS / 32) + k] = ex;
-            ex = v[k] > ex ? v[k] : ex;
-        }
-    }
-    mbar_wait(&S.mbar, 0);
-    __syncthreads();
-    const uint64_t *keys = S.keys + (lo - alo);
-    if (a.dbg == 1) return;
-    // counting-sort slots (Alg. 2)
+    const double rcpF2 = a.rcpF2;
     const Root R = load_root(a.M);
-    uint32_t packed[BS_KPT];
-    uint64_t kv[BS_KPT];
-#pragma unroll
-    for (int j = 0; j < BS_KPT; j++) {
-        const int i = j * bd + tid;
-        packed[j] = 0xffffffffu;
-        if (i < span) {
-            const uint32_t st = head_of(S, (uint32_t)i);
-            const uint32_t gnp = S.gnp[st];
-            const uint32_t g = gnp & 0xfffffu, np = gnp >> 20;
-            const uint64_t key = keys[i];
-            kv[j] = key;
-            uint32_t slot = (uint32_t)i;
-            if ((uint32_t)i - st < np && np >= 2) {
-                const double p = predict_ldg<DT>(key, R, a.M->leaf);
-                const double adj = __ddiv_rn((double)g, a.F2);  // (i*f + j)/f^2
-                slot = st + cs_pos(p, adj, a.nd, (double)(np - 1));
-                if (key != keys[st] && !diff_at(S, st)) atomicOr(&S.diffbits[st >> 5], 1u << (st & 31u));
+    uint32_t phase = 0;
+    uint32_t nx_np = 0, nx_st = 0;
+    // debug (LS_DEBUG_STAGE=256): cycles per phase, thread 0 of every CTA
+    const bool prof = (a.dbg & 256u) && tid == 0;
+    long long t_prev = clock64();
+#define BS_PROF(k)                                                                  \
+    do {                                                                            \
+        if (prof) {                                                                 \
+            const long long t_ = clock64();                                         \
+            atomicAdd(&a.ctl->prof[k], (unsigned long long)(t_ - t_prev));          \
+            t_prev = t_;                                                            \
+        }                                                                           \
+    } while (0)
+    for (uint32_t it = 0;; it++) {
+        const int slot = (int)(it & 1u);
+        // ---- window tables (overlap with the bulk copy in flight)
+        const uint4 desc = S.desc[slot];
+        if (desc.x == BS_NONE) break;
+        const uint32_t g0 = desc.x, g1 = desc.y, lo = desc.z, hi = desc.w;
+        const int span = (int)(hi - lo);
+        uint4 ahead;  // descriptor of window it + 2 (thread 0), in flight meanwhile
+        if (tid == 0) ahead = bs_desc(a, nwin, it + 2);
+        // this window's sub-buckets g0 + tid (prefetched during the previous
+        // window) and the next window's, loaded now for the next iteration
+        uint32_t my_np = 0, my_st = 0;
+        if (it == 0) {
+            if (g0 + tid <= g1) {
+                my_np = __ldg(&a.hist1[g0 + tid]);
+                my_st = __ldg(&a.start1[g0 + tid]);
             }
-            const uint32_t r = atomicAdd(&S.K[slot], 1u);
-            packed[j] = slot | (r << 16);
-        }
-    }
-    __syncthreads();
-    if (a.dbg == 3) return;
-    block_exscan(S.K, span + 1, S.tmp);  // running totals, exclusive (R4)
-    // placement. T holds ord values (plain integer compares in the
-    // touch-up); gnp[q] now remembers the slot of T position q.
-#pragma unroll
-    for (int j = 0; j < BS_KPT; j++) {
-        if (packed[j] == 0xffffffffu) continue;
-        const uint32_t slot = packed[j] & 0xffffu;
-        const uint32_t q = S.K[slot] + (packed[j] >> 16);
-        S.T[q] = to_ord<DT>(kv[j]);
-        S.gnp[q] = slot;
-    }
-    __syncthreads();
-    if (a.dbg == 4) return;
-    // Touch-up per collision group (R15), in T order: every key takes
-    // its rank inside its group (keys strictly below it + equal keys placed
-    // before it) and is stored at its final position -- the insertion sort's
-    // result without its serial shifting. Groups of > 8 keys (typically the
-    // clamped top slot of a sparse sub-bucket, R5) are ordered by a warp.
-    // Only sub-buckets that are not homogeneous are written back.
-    uint32_t maxg = 0;
-    for (int q = tid; q < span; q += bd) {
-        if (!diff_at(S, head_of(S, (uint32_t)q))) continue;  // homogeneous / not counting-sorted
-        const uint32_t slot = S.gnp[q], base = S.K[slot], c = S.K[slot + 1] - base;
-        const uint64_t o = S.T[q];
-        uint32_t fin = (uint32_t)q;
-        if (c > 1) {
-            if ((uint32_t)q == base && c > maxg) maxg = c;
-            if (c <= 8) {
-                uint32_t rank = 0;
-                for (uint32_t k = 0; k < c; k++) {
-                    const uint64_t ok = S.T[base + k];
-                    rank += (ok < o) || (ok == o && base + k < (uint32_t)q);
-                }
-                fin = base + rank;
-            } else {
-                if ((uint32_t)q == base) {
-                    const uint32_t k = atomicAdd(&S.nbig, 1u);
-                    if (k < BS_MAXBIG) S.big[k] = slot;
-                    else S.ovf = 1;
-                }
-                continue;
-            }
-        }
-        a.A[lo + fin] = from_ord<DT>(o);
-    }
-    maxg = (uint32_t)warp_max_u64(maxg);
-    if (lane == 0 && maxg > 1) atomicMax(&S.st_maxg, (unsigned long long)maxg);
-    __syncthreads();
-    if (a.dbg == 5) return;
-    // groups of > 8 keys: one warp each; all-equal groups are stored as they are
-    const uint32_t nb = min(S.nbig, (uint32_t)BS_MAXBIG);
-    for (uint32_t k = warp; k < nb + (S.ovf ? (uint32_t)span : 0u); k += bd >> 5) {
-        uint32_t slot;
-        if (k < nb) {
-            slot = S.big[k];
-        } else {  // overflow: scan all slots (rare)
-            slot = k - nb;
-            const uint32_t c = S.K[slot + 1] - S.K[slot];
-            if (c <= 8 || !diff_at(S, head_of(S, S.K[slot]))) continue;
-            bool listed = false;
-            for (uint32_t q = 0; q < nb; q++) listed |= (S.big[q] == slot);
-            if (listed) continue;
-        }
-        const uint32_t base = S.K[slot], c = S.K[slot + 1] - base;
-        if (c <= 32) {  // register bitonic network across the warp (one key per lane)
-            uint64_t v = (uint32_t)lane < c ? S.T[base + lane] : ~0ull;
-#pragma unroll
-            for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, jj);
-                    const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
-                    v = keep_min ? (w < v ? w : v) : (w > v ? w : v);
-                }
-            }
-            if ((uint32_t)lane < c) a.A[lo + base + lane] = from_ord<DT>(v);
-            continue;
-        }
-        bool same = true;
-        for (uint32_t q = lane; q < c; q += 32) same &= (S.T[base + q] == S.T[base]);
-        if (!__all_sync(0xffffffffu, same)) bitonic<DT_U64, false>(S.T + base, (int)c, lane, 32);
-        for (uint32_t q = lane; q < c; q += 32) a.A[lo + base + q] = from_ord<DT>(S.T[base + q]);
-    }
-    if (a.dbg == 6) return;
-    // per sub-bucket classification: H1 or counting-sorted
-    for (uint32_t g = g0 + tid; g <= g1; g += bd) {
-        const uint32_t np = __ldg(&a.hist1[g]);
-        if (np < 2) continue;
-        if (diff_at(S, __ldg(&a.start1[g]) - lo)) {
-            atomicAdd(&S.st_small, 1ull);
-            atomicAdd(&S.st_smallk, (unsigned long long)np);
         } else {
-            if (a.dH1) a.dH1[g] = 1;
-            atomicAdd(&S.st_h1, 1ull);
-            atomicAdd(&S.st_h1k, (unsigned long long)np);
+            my_np = nx_np;
+            my_st = nx_st;
         }
+        {
+            const uint4 nd = S.desc[slot ^ 1];
+            nx_np = 0;
+            nx_st = 0;
+            if (nd.x != BS_NONE && nd.x + tid <= nd.y) {
+                nx_np = __ldg(&a.hist1[nd.x + tid]);
+                nx_st = __ldg(&a.start1[nd.x + tid]);
+            }
+        }
+        {
+            uint4 *k4 = reinterpret_cast<uint4 *>(S.K);
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            for (int i = tid; i < (span + 4) / 4 + 1; i += BS_THREADS) k4[i] = z;
+            if (tid < BS_WORDS) S.headbits[tid] = S.wbits[tid] = 0;
+            if (tid == 0) S.nbig = S.ovf = 0;
+        }
+        __syncthreads();
+        BS_PROF(0);
+        for (uint32_t g = g0 + tid; g <= g1; g += BS_THREADS) {  // the window's sub-buckets
+            const bool first = g == g0 + tid;
+            const uint32_t np = first ? my_np : __ldg(&a.hist1[g]);
+            if (np >= 1) {
+                const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
+                atomicOr(&S.headbits[h >> 5], 1u << (h & 31u));
+                S.gnp[h] = g | ((np - 1u) << 20);
+            }
+        }
+        __syncthreads();
+        BS_PROF(1);
+        if (warp == 0) {  // wlast: exclusive max-scan over the per-word last heads
+            uint32_t v[BS_WORDS / 32];
+            uint32_t run = 0;
+            static_assert(BS_WORDS % 32 == 0, "wlast layout");
+#pragma unroll
+            for (int k = 0; k < BS_WORDS / 32; k++) {
+                const int w = lane * (BS_WORDS / 32) + k;
+                const uint32_t b = S.headbits[w];
+                v[k] = b ? (uint32_t)(w << 5) + 32u - __clz(b) : 0u;
+                run = v[k] > run ? v[k] : run;
+            }
+            uint32_t ex = __shfl_up_sync(0xffffffffu, warp_incl_max(run), 1);
+            if (lane == 0) ex = 0;
+#pragma unroll
+            for (int k = 0; k < BS_WORDS / 32; k++) {
+                S.wlast[lane * (BS_WORDS / 32) + k] = ex;
+                ex = v[k] > ex ? v[k] : ex;
+            }
+        }
+        mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
+        __syncthreads();
+        BS_PROF(2);
+        // ---- counting-sort slots (Alg. 2)
+        const uint64_t *keys = S.ring[slot] + (lo & 1u);
+        uint64_t key[BS_KPT];
+        uint32_t code[BS_KPT];  // slot | r << BS_LOG_W
+#pragma unroll
+        for (int k = 0; k < BS_KPT; k++) {
+            const int i = k * BS_THREADS + tid;
+            code[k] = BS_NONE;
+            if (i < span) {
+                const uint32_t h = head_of(S, (uint32_t)i);
+                const uint32_t e = S.gnp[h];
+                const uint32_t np = (e >> 20) + 1u;
+                key[k] = keys[i];
+                uint32_t sl = (uint32_t)i;
+                // (keys of a homogeneous level-0 bucket lying inside the span
+                // have no head of their own: they stay where they are)
+                if (np >= 2u && (uint32_t)i - h < np) {
+                    const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
+                    const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
+                    sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
+                }
+                const uint32_t r = atomicAdd(&S.K[sl], 1u);
+                code[k] = sl | (r << BS_LOG_W);
+            }
+        }
+        __syncthreads();
+        BS_PROF(3);
+        // running totals, exclusive (R4): 8 consecutive entries per
+        // thread; collision groups of more than BS_RANKMAX keys are listed here
+        static_assert(BS_KPT == 8, "scan layout");
+        {
+            uint4 *k4 = reinterpret_cast<uint4 *>(S.K) + 2 * tid;
+            uint4 x0 = k4[0], x1 = k4[1];
+            uint32_t v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            uint32_t sum = 0, mg = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                // entries past the span hold stale totals of an earlier window
+                const uint32_t t = 8 * tid + q < span ? v[q] : 0u;
+                mg = t > mg ? t : mg;
+                if (t > BS_RANKMAX) {
+                    const uint32_t j = atomicAdd(&S.nbig, 1u);
+                    if (j < BS_MAXBIG) S.big[j] = 8u * tid + q; else S.ovf = 1;
+                }
+                v[q] = sum;
+                sum += t;
+            }
+            mg = __reduce_max_sync(0xffffffffu, mg);
+            if (lane == 0 && mg > 1u) atomicMax(&S.st_maxg, (unsigned long long)mg);
+            const uint32_t incl = warp_incl_scan(sum);
+            if (lane == 31) S.wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < BS_THREADS / 32 ? S.wsum[lane] : 0u;
+                S.wsum[lane] = warp_incl_scan(w) - w;
+            }
+            __syncthreads();
+            const uint32_t off = S.wsum[warp] + incl - sum;
+            k4[0] = make_uint4(v[0] + off, v[1] + off, v[2] + off, v[3] + off);
+            k4[1] = make_uint4(v[4] + off, v[5] + off, v[6] + off, v[7] + off);
+        }
+        __syncthreads();
+        BS_PROF(4);
+        // placement: T = the consumed slot, holding ord values;
+        // slot_of[q] remembers the slot of T position q
+        uint64_t *T = S.ring[slot];
+#pragma unroll
+        for (int k = 0; k < BS_KPT; k++) {
+            if (code[k] != BS_NONE) {
+                const uint32_t sl = code[k] & (BS_W - 1u);
+                const uint32_t q = S.K[sl] + (code[k] >> BS_LOG_W);
+                T[q] = to_ord<DT>(key[k]);
+                S.slot_of[q] = (uint16_t)sl;
+            }
+        }
+        __syncthreads();
+        BS_PROF(5);
+        // Touch-up per collision group (R15). T is in slot order, so a
+        // group is a run of equal slot_of. Each thread owns 8 consecutive
+        // positions and runs odd-even transposition rounds that only exchange
+        // neighbours of equal slot (neighbouring threads via shuffles) until a
+        // round pair swaps nothing in the warp; <= 8 rounds sort every group of
+        // <= 8 keys inside a warp's 256 positions. Groups > 8 (listed by the
+        // scan) and groups straddling two warps are sorted by a warp below.
+        {
+            const uint32_t q0 = 8u * tid;
+            uint64_t v[8];
+            uint32_t sv[8];
+            {
+                const uint4 *t4 = reinterpret_cast<const uint4 *>(T + q0);
+                const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * tid];
+                const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * tid + 1];
+                const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const bool in = q0 + q < (uint32_t)span;
+                    const uint4 t = t4[q >> 1];
+                    const uint64_t val = (q & 1) ? ((uint64_t)t.w << 32 | t.z) : ((uint64_t)t.y << 32 | t.x);
+                    v[q] = in ? val : ~0ull;
+                    sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
+                }
+            }
+            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
+                const bool sw_ = sx == sy && x > y;
+                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
+                x = lo_;
+                y = hi_;
+                return sw_;
+            };
+            for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
+                bool any = false;
+                any |= cx(v[0], v[1], sv[0], sv[1]);
+                any |= cx(v[2], v[3], sv[2], sv[3]);
+                any |= cx(v[4], v[5], sv[4], sv[5]);
+                any |= cx(v[6], v[7], sv[6], sv[7]);
+                any |= cx(v[1], v[2], sv[1], sv[2]);
+                any |= cx(v[3], v[4], sv[3], sv[4]);
+                any |= cx(v[5], v[6], sv[5], sv[6]);
+                const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
+                const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
+                const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
+                const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
+                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                if (!__any_sync(0xffffffffu, any)) break;
+            }
+            uint4 *t4 = reinterpret_cast<uint4 *>(T + q0);
+            if (q0 < (uint32_t)span) {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    t4[q] = make_uint4((uint32_t)v[2 * q], (uint32_t)(v[2 * q] >> 32),
+                                       (uint32_t)v[2 * q + 1], (uint32_t)(v[2 * q + 1] >> 32));
+            }
+            // a small group straddling two warps' ranges: list it for a warp
+            if (lane == 0 && warp > 0 && q0 < (uint32_t)span && sv[0] < 0x10000u &&
+                S.slot_of[q0 - 1] == sv[0]) {
+                const uint32_t sl = sv[0], c = S.K[sl + 1] - S.K[sl];
+                if (c <= BS_RANKMAX) {
+                    const uint32_t j = atomicAdd(&S.nbig, 1u);
+                    if (j < BS_MAXBIG) S.big[j] = sl; else S.ovf = 1;
+                }
+            }
+        }
+        __syncthreads();
+        BS_PROF(6);
+        // one warp per listed group: register bitonic (<= 32 / <= 64 keys) or
+        // shared-memory bitonic; all-equal groups are left alone
+        {
+            const uint32_t nb = min(S.nbig, (uint32_t)BS_MAXBIG);
+            const uint32_t extra = S.ovf ? (uint32_t)span : 0u;
+            for (uint32_t k = warp; k < nb + extra; k += BS_THREADS / 32) {
+                uint32_t sl;
+                if (k < nb) {
+                    sl = S.big[k];
+                } else {  // overflow: sort every multi-key group again (rare; idempotent)
+                    sl = k - nb;
+                    if (S.K[sl + 1] - S.K[sl] < 2u) continue;
+                }
+                const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
+                if ((a.dbg & 256u) && lane == 0)
+                    atomicAdd(&a.ctl->prof[c <= 16 ? 10 : c <= 32 ? 11 : c <= 64 ? 12 : c <= 256 ? 13 : c <= 1024 ? 14 : 15], 1ull);
+                if (c <= BS_RANKMAX) {  // a small group straddling two warps: one lane
+                    if (lane == 0) {
+                        for (uint32_t x = 1; x < c; x++) {
+                            const uint64_t t = T[base + x];
+                            uint32_t y = x;
+                            while (y > 0 && T[base + y - 1] > t) {
+                                T[base + y] = T[base + y - 1];
+                                y--;
+                            }
+                            T[base + y] = t;
+                        }
+                    }
+                    continue;
+                }
+                bool same = true;
+                for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
+                if (__all_sync(0xffffffffu, same)) continue;
+                if (c <= 32u) {  // register bitonic across the warp
+                    uint64_t v = (uint32_t)lane < c ? T[base + lane] : ~0ull;
+                    warp_sort32(v, lane);
+                    if ((uint32_t)lane < c) T[base + lane] = v;
+                } else if (c <= 64u) {
+                    uint64_t v[2];
+                    v[0] = T[base + lane];
+                    v[1] = (uint32_t)lane + 32u < c ? T[base + 32 + lane] : ~0ull;
+                    warp_sort64(v, lane);
+                    T[base + lane] = v[0];
+                    if ((uint32_t)lane + 32u < c) T[base + 32 + lane] = v[1];
+                } else {
+                    bitonic<DT_U64, false>(T + base, (int)c, lane, 32);
+                }
+            }
+        }
+        __syncthreads();
+        BS_PROF(7);
+        // per sub-bucket classification: H1 or counting-sorted; the
+        // latter are marked for the store-back
+        for (uint32_t g = g0 + tid; g <= g1; g += BS_THREADS) {
+            const bool first = g == g0 + tid;
+            const uint32_t np = first ? my_np : __ldg(&a.hist1[g]);
+            if (np < 2) continue;
+            const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
+            if (T[h] != T[h + np - 1u]) {  // sorted: homogeneous iff first == last
+                atomicAdd(&S.st_small, 1ull);
+                atomicAdd(&S.st_smallk, (unsigned long long)np);
+                const uint32_t e = h + np;  // set bits [h, e)
+                for (uint32_t w = h >> 5; w <= (e - 1) >> 5; w++) {
+                    const uint32_t b0 = w == (h >> 5) ? (h & 31u) : 0u;
+                    const uint32_t b1 = w == ((e - 1) >> 5) ? ((e - 1) & 31u) : 31u;
+                    const uint32_t m = (0xffffffffu >> (31u - b1)) & (0xffffffffu << b0);
+                    atomicOr(&S.wbits[w], m);
+                }
+            } else {
+                if (a.dH1) a.dH1[g] = 1;
+                atomicAdd(&S.st_h1, 1ull);
+                atomicAdd(&S.st_h1k, (unsigned long long)np);
+            }
+        }
+        __syncthreads();
+        BS_PROF(8);
+        // store back (coalesced), skipping keys that are already in place
+        for (int q = tid; q < span; q += BS_THREADS)
+            if ((S.wbits[q >> 5] >> (q & 31)) & 1u) a.A[lo + q] = from_ord<DT>(T[q]);
+        __syncthreads();
+        BS_PROF(9);
+        phase ^= 1u << slot;
+        if (tid == 0) bs_stage(S, slot, a, ahead);
     }
     __syncthreads();
     if (tid == 0) {
@@ -311,18 +539,23 @@ __global__ void __launch_bounds__(BS_THREADS, 2) k_bucketsort(Args a) {
     }
 }
 
-// {g0, g1, lo, hi} per bucket-sort window: one dependent load per CTA instead
-// of two chained ones on the critical path of every tile.
-__global__ void k_tile_desc(Args a) {
+// Compact the non-empty windows into wlist: {g0, g1, lo, hi}.
+__global__ void k_window_list(Args a) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.ntiles) return;
-    const uint32_t g0 = a.tile_first[t];
-    uint4 d = make_uint4(0xffffffffu, 0u, 0u, 0u);
-    if (g0 != 0xffffffffu) {
-        const uint32_t g1 = a.tile_last[t];
-        d = make_uint4(g0, g1, a.start1[g0], a.start1[g1] + a.hist1[g1]);
+    uint4 d = make_uint4(BS_NONE, 0u, 0u, 0u);
+    if (t < a.ntiles) {
+        const uint32_t g0 = a.tile_first[t];
+        if (g0 != BS_NONE) {
+            const uint32_t g1 = a.tile_last[t];
+            d = make_uint4(g0, g1, a.start1[g0], a.start1[g1] + a.hist1[g1]);
+        }
     }
-    a.tdesc[t] = d;
+    const bool has = d.x != BS_NONE;
+    const uint32_t m = __ballot_sync(0xffffffffu, has);
+    uint32_t base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&a.ctl->nwin, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (has) a.wlist[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = d;
 }
 
 // ------------------------------------------------------------- BIG path ----
@@ -590,14 +823,18 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
 
 // -------------------------------------------------------------- launchers --
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
-    k_tile_desc<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
+    k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)umin64((uint64_t)sms * BS_CTAS_PER_SM, a.ntiles);
     if (dtype == DT_F64) {
         cudaFuncSetAttribute(k_bucketsort<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_bucketsort<DT_F64><<<a.ntiles, BS_THREADS, sm, st>>>(a);
+        k_bucketsort<DT_F64><<<grid, BS_THREADS, sm, st>>>(a);
     } else {
         cudaFuncSetAttribute(k_bucketsort<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_bucketsort<DT_U64><<<a.ntiles, BS_THREADS, sm, st>>>(a);
+        k_bucketsort<DT_U64><<<grid, BS_THREADS, sm, st>>>(a);
     }
 }
 
