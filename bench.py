@@ -70,7 +70,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi has produced its first sample (it takes a
+        few hundred ms to start), so the timed region is actually sampled."""
+        t0 = time.monotonic()
+        while self.proc and not self.lines and time.monotonic() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self, name):
+        setattr(self, name, time.monotonic())
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,7 +93,9 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t_start", None), getattr(self, "t_end", None)
+        inside = [ln for t, ln in self.lines if t0 is None or (t0 <= t <= t1 + 0.05)]
+        for ln in inside or [ln for _, ln in self.lines[-3:]]:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -202,14 +214,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     times, stats = [], []
     with ClockSampler(local) as clk:
+        clk.wait_first()
         if multi:
             dist.barrier()
         torch.cuda.synchronize()
+        clk.mark("t_start")
         for _ in range(args.steps):
             ms, st, n_out = one_step()
             times.append(ms)
             stats.append(st)
         torch.cuda.synchronize()
+        clk.mark("t_end")
         if multi:
             dist.barrier()
     total_ms = sum(times)

@@ -289,7 +289,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         launches += 3;
     }
     launch_b0_table(a.M, l.L, l.f, dt, st);
-    launches++;
+    launches += 2;
     tm.mark(LS_PHASE_FIT);
     launch_count0(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, st);
