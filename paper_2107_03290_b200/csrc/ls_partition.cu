@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
     tp_init(S.tp);
     const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
     uint32_t phase = 0;
-    tile_partition(S.tp, a.A, a.B, beg, end, S.base, f, bf, phase);
+    tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase);
 }
 
 // --------------------------------------------------------------- round 1 ---
@@ -223,13 +223,39 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     const uint64_t end = umin64(bend, beg + a.C1);
     const Root R = load_root(a.M);
     unsigned long long mn = ~0ull, mx = 0;
-    for (uint64_t i = beg + tid; i < end; i += bd) {
-        const uint64_t key = a.B[i];
+    auto one = [&](uint64_t key) {
         const unsigned long long o = to_ord<DT>(key);
         mn = o < mn ? o : mn;
         mx = o > mx ? o : mx;
         const double p = predict_ldg<DT>(key, R, a.M->leaf);
         atomicAdd(&hist[bucket1(p, a.F2, f, (uint32_t)b)], 1u);
+    };
+    {
+        // 16-byte loads, 4 in flight per thread; odd head / tail keys apart
+        uint64_t i0 = beg;
+        if ((i0 & 1) && i0 < end) {
+            if (tid == 0) one(a.B[i0]);
+            i0++;
+        }
+        const ulonglong2 *B2 = reinterpret_cast<const ulonglong2 *>(a.B + i0);
+        const uint64_t np = (end - i0) / 2;
+        uint64_t i = tid;
+        for (; i + 3 * bd < np; i += 4 * bd) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = __ldcs(B2 + i + q * bd);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                one(v[q].x);
+                one(v[q].y);
+            }
+        }
+        for (; i < np; i += bd) {
+            const ulonglong2 v = __ldcs(B2 + i);
+            one(v.x);
+            one(v.y);
+        }
+        if (((end - i0) & 1) && tid == 0) one(a.B[end - 1]);
     }
     mn = warp_min_u64(mn);
     mx = warp_max_u64(mx);
@@ -290,7 +316,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     tp_init(S.tp);
     const ModelBucket<DT, 1, false> bf{load_root(a.M), a.M->leaf, a.F, a.F2, f, (uint32_t)b};
     uint32_t phase = 0;
-    tile_partition(S.tp, a.B, a.A, beg, end, S.base, f, bf, phase);
+    tile_partition(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase);
 }
 
 // ------------------------------------------------------------- classify ----

@@ -68,6 +68,49 @@ __device__ __forceinline__ void bitonic(uint64_t *g, int c, int lane, int lanes)
     }
 }
 
+// Bitonic over an indexable view (same network as bitonic()).
+template <class V>
+__device__ __forceinline__ void bitonic_view(V g, int c, int lane, int lanes) {
+    int P = 1, lg = 0;
+    while (P < c) { P <<= 1; lg++; }
+    const int halfP = P >> 1;
+    auto cs = [&](int lo, int hi) {
+        const uint64_t x = g[lo], y = g[hi];
+        if (x > y) { g[lo] = y; g[hi] = x; }
+    };
+    for (int lk = 1; lk <= lg; lk++) {
+        const int k = 1 << lk, lh = lk - 1;
+        for (int i = lane; i < halfP; i += lanes) {
+            const int blk = i >> lh, p = i & ((1 << lh) - 1);
+            const int lo = blk * k + p, hi = blk * k + k - 1 - p;
+            if (hi < c) cs(lo, hi);
+        }
+        __syncwarp();
+        for (int lj = lk - 2; lj >= 0; lj--) {
+            const int j = 1 << lj;
+            for (int i = lane; i < halfP; i += lanes) {
+                const int blk = i >> lj, p = i & (j - 1);
+                const int lo = blk * 2 * j + p, hi = lo + j;
+                if (hi < c) cs(lo, hi);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// T in shared memory with one pad word per 8: position q lives at q + q/8, so
+// a thread reading its 8 consecutive positions (odd-even phase) and a warp
+// reading 32 consecutive positions (store-back) are both bank-conflict free.
+struct PadT {
+    uint64_t *p;
+    uint32_t off;  // view offset (positions)
+    __device__ __forceinline__ uint64_t &operator[](uint32_t q) const {
+        const uint32_t x = q + off;
+        return p[x + (x >> 3)];
+    }
+    __device__ __forceinline__ PadT operator+(uint32_t d) const { return PadT{p, off + d}; }
+};
+
 // ----------------------------------------------------------- SMALL path ----
 // Windows: classify assigns every SMALL sub-bucket (2 <= n' <= T_small) to the
 // window of T_tile positions its start falls in (T_tile <= T_small), so a
@@ -103,10 +146,11 @@ constexpr uint32_t BS_RANKMAX = 8;         // groups up to this size: owner-thre
 constexpr uint32_t BS_NONE = 0xffffffffu;
 
 struct BsSmem {
-    uint64_t ring[2][BS_W + 2];             // staged spans; the current one becomes T
+    uint64_t ring[2][BS_W + BS_W / 8];      // staged spans; the current one becomes T (padded)
     alignas(16) uint32_t K[BS_W + 4];       // slot histogram -> exclusive running totals
-    uint32_t gnp[BS_W];                     // at a head: g | (n' - 1) << 20
-    uint16_t slot_of[BS_W];                 // after placement: slot of T position q
+    uint32_t gnp[BS_W];                     // at a head: g | (n' - 1) << 20; after
+                                            // placement its storage is slot_of[] (u16):
+                                            // the slot of T position q
     uint32_t headbits[BS_WORDS];            // sub-bucket heads (bit per position)
     uint32_t wlast[BS_WORDS];               // 1 + last head position before word w (0: none)
     uint32_t wbits[BS_WORDS];               // positions to store back (non-homogeneous SMALL sub-buckets)
@@ -125,18 +169,23 @@ __device__ __forceinline__ uint32_t head_of(const BsSmem &S, uint32_t q) {
     return bits ? (w << 5) + 31u - __clz(bits) : S.wlast[w] - 1u;
 }
 
-// Stage A[lo, hi) into ring slot `slot` (key k at slot[k - (lo & ~1)]); thread 0 only.
+// Stage A[lo, hi) into ring slot `slot` (key k at slot[k - (lo & ~1)]); thread
+// 0 only. The bulk copy covers the 16-byte-aligned hull; only if that would run
+// past the end of A is the last key loaded directly.
 __device__ __forceinline__ void bs_issue(BsSmem &S, int slot, const uint64_t *A, uint32_t lo,
-                                         uint32_t hi) {
+                                         uint32_t hi, uint64_t n) {
     uint64_t *dst = S.ring[slot];
-    const uint32_t a0 = lo & ~1u, ilo = (lo + 1) & ~1u, ihi = hi & ~1u;
-    if (lo & 1u) dst[lo - a0] = A[lo];
-    if ((hi & 1u) && hi - 1 >= ilo) dst[hi - 1 - a0] = A[hi - 1];
-    const uint32_t bytes = ihi > ilo ? (ihi - ilo) * 8u : 0u;
+    const uint32_t a0 = lo & ~1u;
+    uint32_t a1 = (hi + 1u) & ~1u;
+    if (a1 > n) {
+        a1 = hi & ~1u;
+        dst[hi - 1 - a0] = A[hi - 1];
+    }
+    const uint32_t bytes = a1 > a0 ? (a1 - a0) * 8u : 0u;
     mbar_expect_tx(&S.mbar[slot], bytes);
     for (uint32_t o = 0; o < bytes; o += 32768u)
-        bulk_g2s((char *)(dst + (ilo - a0)) + o, (const char *)(A + ilo) + o,
-                 bytes - o < 32768u ? bytes - o : 32768u, &S.mbar[slot]);
+        bulk_g2s((char *)dst + o, (const char *)(A + a0) + o, bytes - o < 32768u ? bytes - o : 32768u,
+                 &S.mbar[slot]);
 }
 
 // Stage window descriptor d into `slot` (thread 0); the end of the CTA's
@@ -144,7 +193,7 @@ __device__ __forceinline__ void bs_issue(BsSmem &S, int slot, const uint64_t *A,
 // the wait completes.
 __device__ __forceinline__ void bs_stage(BsSmem &S, int slot, const Args &a, uint4 d) {
     S.desc[slot] = d;
-    if (d.x != BS_NONE) bs_issue(S, slot, a.A, d.z, d.w);
+    if (d.x != BS_NONE) bs_issue(S, slot, a.A, d.z, d.w, a.n);
     else mbar_expect_tx(&S.mbar[slot], 0u);
 }
 // CTA c sorts windows c, c + G, c + 2G, ... (G = gridDim.x): no ticket on the
@@ -217,6 +266,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
     const Root R = load_root(a.M);
     uint32_t phase = 0;
     uint32_t nx_np = 0, nx_st = 0;
+    unsigned long long r_small = 0, r_smallk = 0, r_h1 = 0, r_h1k = 0;  // stats (per thread)
     // debug (LS_DEBUG_STAGE=256): cycles per phase, thread 0 of every CTA
     const bool prof = (a.dbg & 256u) && tid == 0;
     long long t_prev = clock64();
@@ -365,14 +415,15 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         BS_PROF(4);
         // placement: T = the consumed slot, holding ord values;
         // slot_of[q] remembers the slot of T position q
-        uint64_t *T = S.ring[slot];
+        const PadT T{S.ring[slot], 0u};
+        uint16_t *slot_of = reinterpret_cast<uint16_t *>(S.gnp);
 #pragma unroll
         for (int k = 0; k < BS_KPT; k++) {
             if (code[k] != BS_NONE) {
                 const uint32_t sl = code[k] & (BS_W - 1u);
                 const uint32_t q = S.K[sl] + (code[k] >> BS_LOG_W);
                 T[q] = to_ord<DT>(key[k]);
-                S.slot_of[q] = (uint16_t)sl;
+                slot_of[q] = (uint16_t)sl;
             }
         }
         __syncthreads();
@@ -389,16 +440,14 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
             uint64_t v[8];
             uint32_t sv[8];
             {
-                const uint4 *t4 = reinterpret_cast<const uint4 *>(T + q0);
-                const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * tid];
-                const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * tid + 1];
+                const uint2 s2 = reinterpret_cast<const uint2 *>(slot_of)[2 * tid];
+                const uint2 s3 = reinterpret_cast<const uint2 *>(slot_of)[2 * tid + 1];
                 const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
+                const uint64_t *row = S.ring[slot] + 9u * tid;  // = &T[q0] (padded)
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const bool in = q0 + q < (uint32_t)span;
-                    const uint4 t = t4[q >> 1];
-                    const uint64_t val = (q & 1) ? ((uint64_t)t.w << 32 | t.z) : ((uint64_t)t.y << 32 | t.x);
-                    v[q] = in ? val : ~0ull;
+                    v[q] = in ? row[q] : ~0ull;
                     sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
                 }
             }
@@ -426,16 +475,14 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
                 if (!__any_sync(0xffffffffu, any)) break;
             }
-            uint4 *t4 = reinterpret_cast<uint4 *>(T + q0);
             if (q0 < (uint32_t)span) {
+                uint64_t *row = S.ring[slot] + 9u * tid;
 #pragma unroll
-                for (int q = 0; q < 4; q++)
-                    t4[q] = make_uint4((uint32_t)v[2 * q], (uint32_t)(v[2 * q] >> 32),
-                                       (uint32_t)v[2 * q + 1], (uint32_t)(v[2 * q + 1] >> 32));
+                for (int q = 0; q < 8; q++) row[q] = v[q];
             }
             // a small group straddling two warps' ranges: list it for a warp
             if (lane == 0 && warp > 0 && q0 < (uint32_t)span && sv[0] < 0x10000u &&
-                S.slot_of[q0 - 1] == sv[0]) {
+                slot_of[q0 - 1] == sv[0]) {
                 const uint32_t sl = sv[0], c = S.K[sl + 1] - S.K[sl];
                 if (c <= BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
@@ -490,7 +537,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                     T[base + lane] = v[0];
                     if ((uint32_t)lane + 32u < c) T[base + 32 + lane] = v[1];
                 } else {
-                    bitonic<DT_U64, false>(T + base, (int)c, lane, 32);
+                    bitonic_view(T + base, (int)c, lane, 32);
                 }
             }
         }
@@ -504,8 +551,8 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
             if (np < 2) continue;
             const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
             if (T[h] != T[h + np - 1u]) {  // sorted: homogeneous iff first == last
-                atomicAdd(&S.st_small, 1ull);
-                atomicAdd(&S.st_smallk, (unsigned long long)np);
+                r_small++;
+                r_smallk += np;
                 const uint32_t e = h + np;  // set bits [h, e)
                 for (uint32_t w = h >> 5; w <= (e - 1) >> 5; w++) {
                     const uint32_t b0 = w == (h >> 5) ? (h & 31u) : 0u;
@@ -515,8 +562,8 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 }
             } else {
                 if (a.dH1) a.dH1[g] = 1;
-                atomicAdd(&S.st_h1, 1ull);
-                atomicAdd(&S.st_h1k, (unsigned long long)np);
+                r_h1++;
+                r_h1k += np;
             }
         }
         __syncthreads();
@@ -529,6 +576,10 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         phase ^= 1u << slot;
         if (tid == 0) bs_stage(S, slot, a, ahead);
     }
+    if (r_small) atomicAdd(&S.st_small, r_small);
+    if (r_smallk) atomicAdd(&S.st_smallk, r_smallk);
+    if (r_h1) atomicAdd(&S.st_h1, r_h1);
+    if (r_h1k) atomicAdd(&S.st_h1k, r_h1k);
     __syncthreads();
     if (tid == 0) {
         if (S.st_small) atomicAdd(&a.ctl->stat[ST_SMALLS], S.st_small);

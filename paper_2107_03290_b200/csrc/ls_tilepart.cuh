@@ -39,38 +39,43 @@ struct TpSmem {
 };
 
 // Issue the bulk copy of src[t0, t1) into ring slot `slot`, so that key k lands
-// at slot[k - (t0 & ~1)]. The bulk engine moves the 16-byte-aligned interior;
-// an odd first / last key is loaded by this (single) thread directly.
+// at slot[k - (t0 & ~1)]. The bulk engine moves 16-byte-aligned ranges, so the
+// copy covers the aligned hull [t0 & ~1, (t1 + 1) & ~1); only when that hull
+// would run past the end of the array (len odd, t1 == len) is the last key
+// loaded by this (single) thread directly.
 __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *src, uint64_t t0,
-                                         uint64_t t1) {
+                                         uint64_t t1, uint64_t len) {
     uint64_t *dst = S.ring[slot];
     const uint64_t a0 = t0 & ~1ull;
-    const uint64_t lo = (t0 + 1) & ~1ull, hi = t1 & ~1ull;  // aligned interior [lo, hi)
-    if (t0 & 1) dst[t0 - a0] = src[t0];                              // odd head
-    if ((t1 & 1) && t1 - 1 >= lo) dst[t1 - 1 - a0] = src[t1 - 1];    // odd tail
-    const uint32_t bytes = hi > lo ? (uint32_t)((hi - lo) * 8) : 0u;
+    uint64_t a1 = (t1 + 1) & ~1ull;
+    if (a1 > len) {
+        a1 = t1 & ~1ull;
+        dst[t1 - 1 - a0] = src[t1 - 1];
+    }
+    const uint32_t bytes = a1 > a0 ? (uint32_t)((a1 - a0) * 8) : 0u;
     mbar_expect_tx(&S.mbar[slot], bytes);
     constexpr uint32_t CH = 32768;
     for (uint32_t o = 0; o < bytes; o += CH)
-        bulk_g2s((char *)(dst + (lo - a0)) + o, (const char *)(src + lo) + o,
-                 bytes - o < CH ? bytes - o : CH, &S.mbar[slot]);
+        bulk_g2s((char *)dst + o, (const char *)(src + a0) + o, bytes - o < CH ? bytes - o : CH,
+                 &S.mbar[slot]);
 }
 
 // Partition src[beg, end) into nb <= 1024 buckets: key -> dst[base[b]++].
+// len = number of keys in the src array (bound for the aligned hull).
 // base[] is in shared memory, owned by thread b. bf(key, index) -> bucket.
 // All threads of the CTA call it; S.mbar must have been initialised (count 1)
 // by tp_init and every phase used so far is tracked in `phase`.
 template <class BF>
 __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
-                                               uint64_t end, uint32_t *base, int nb,
-                                               const BF &bf, uint32_t &phase) {
+                                               uint64_t end, uint64_t len, uint32_t *base,
+                                               int nb, const BF &bf, uint32_t &phase) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
     if (ntl == 0) return;
     if (tid == 0) {
-        tp_issue(S, 0, src, beg, umin64(end, beg + TP_TILE));
-        if (ntl > 1) tp_issue(S, 1, src, beg + TP_TILE, umin64(end, beg + 2 * TP_TILE));
+        tp_issue(S, 0, src, beg, umin64(end, beg + TP_TILE), len);
+        if (ntl > 1) tp_issue(S, 1, src, beg + TP_TILE, umin64(end, beg + 2 * TP_TILE), len);
     }
     if (tid < nb) S.cnt[tid] = 0;
     __syncthreads();
@@ -113,27 +118,42 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             S.cnt[tid] = 0;
         }
         __syncthreads();
-        // bucket-contiguous order inside the consumed slot
+        // bucket-contiguous order inside the consumed slot (all lookups
+        // first, then all stores: independent shared-memory chains)
         uint64_t *sk = S.ring[slot];
+        uint32_t pos[TP_KPT];
+#pragma unroll
+        for (int k = 0; k < TP_KPT; k++)
+            pos[k] = code[k] != 0xffffffffu ? S.ex[code[k] & 1023u] + (code[k] >> 10) : 0xffffffffu;
 #pragma unroll
         for (int k = 0; k < TP_KPT; k++) {
-            if (code[k] != 0xffffffffu) {
-                const uint32_t b = code[k] & 1023u;
-                const uint32_t pos = S.ex[b] + (code[k] >> 10);
-                sk[pos] = key[k];
-                S.sbin[pos] = (uint16_t)b;
+            if (pos[k] != 0xffffffffu) {
+                sk[pos[k]] = key[k];
+                S.sbin[pos[k]] = (uint16_t)(code[k] & 1023u);
             }
         }
         __syncthreads();
-#pragma unroll 4
-        for (int idx = tid; idx < tn; idx += TP_THREADS) {
-            const uint32_t b = S.sbin[idx];
-            dst[S.delta[b] + (uint32_t)idx] = sk[idx];
+        {
+            uint32_t b[TP_KPT], d[TP_KPT];
+            uint64_t v[TP_KPT];
+#pragma unroll
+            for (int k = 0; k < TP_KPT; k++) {
+                const int idx = k * TP_THREADS + tid;
+                b[k] = idx < tn ? S.sbin[idx] : 0u;
+                v[k] = sk[idx];
+            }
+#pragma unroll
+            for (int k = 0; k < TP_KPT; k++) d[k] = S.delta[b[k]];
+#pragma unroll
+            for (int k = 0; k < TP_KPT; k++) {
+                const int idx = k * TP_THREADS + tid;
+                if (idx < tn) dst[d[k] + (uint32_t)idx] = v[k];
+            }
         }
         __syncthreads();
         phase ^= 1u << slot;
         if (tid == 0 && i + 2 < ntl)
-            tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE));
+            tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE), len);
     }
 }
 
