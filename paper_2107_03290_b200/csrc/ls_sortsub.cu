@@ -142,7 +142,7 @@ constexpr int BS_LOG_W = 11;
 static_assert((1 << BS_LOG_W) == BS_W, "BS_LOG_W");
 constexpr int BS_CTAS_PER_SM = 4;
 constexpr int BS_MAXBIG = 256;             // collision groups > BS_RANKMAX keys per window
-constexpr uint32_t BS_RANKMAX = 8;         // groups up to this size: owner-thread ranks
+constexpr uint32_t BS_RANKMAX = 8;         // groups up to this size: odd-even rounds
 constexpr uint32_t BS_NONE = 0xffffffffu;
 
 struct BsSmem {
@@ -244,6 +244,56 @@ __device__ __forceinline__ void warp_sort64(uint64_t v[2], int lane) {
                 }
             }
         }
+    }
+}
+
+// Ascending bitonic sort of 32*NS ord values across a warp, in registers:
+// element i = 32*s + lane lives in v[s]. Partners at distance >= 32 are in the
+// same lane (register compare-exchange), closer ones are one shuffle away.
+template <int NS>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[NS], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32 * NS; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj >= 32) {
+                const int js = jj >> 5;
+#pragma unroll
+                for (int s2 = 0; s2 < NS; s2++) {
+                    if (s2 & js) continue;
+                    const int i = 32 * s2 + lane;
+                    const bool asc = (i & kk) == 0;
+                    const uint64_t x = v[s2], y = v[s2 | js];
+                    const bool sw_ = asc ? (x > y) : (x < y);
+                    v[s2] = sw_ ? y : x;
+                    v[s2 | js] = sw_ ? x : y;
+                }
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < NS; s2++) {
+                    const int i = 32 * s2 + lane;
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
+                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
+                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
+                }
+            }
+        }
+    }
+}
+
+template <int DT, int NS>
+__device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int lane) {
+    uint64_t v[NS];
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        v[s2] = i < pc ? to_ord<DT>(g[i]) : ~0ull;
+    }
+    warp_sort_regs<NS>(v, lane);
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        if (i < pc) g[i] = from_ord<DT>(v[s2]);
     }
 }
 
@@ -722,6 +772,16 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
     const int nwarps = bd >> 5;
     const uint32_t cnt = min(a.ctl->big_cnt[level], a.big_cap);
     const BigItem *list = a.big + (size_t)level * a.big_cap;
+    const bool prof = (a.dbg & 512u) && threadIdx.x == 0;
+    long long t_prev = clock64();
+#define BG_PROF(k)                                                                  \
+    do {                                                                            \
+        if (prof) {                                                                 \
+            const long long t_ = clock64();                                         \
+            atomicAdd(&a.ctl->prof[k], (unsigned long long)(t_ - t_prev));          \
+            t_prev = t_;                                                            \
+        }                                                                           \
+    } while (0)
     for (;;) {
         if (tid == 0) S.item = atomicAdd(&a.ctl->big_next[level], 1u);
         __syncthreads();
@@ -765,6 +825,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
             __syncthreads();
             continue;
         }
+        BG_PROF(0);
         // MSD radix partition X -> Y on the top 12 bits of ord - mn
         const unsigned long long range = mx - mn;
         const int bits = 64 - __clzll((long long)range);
@@ -782,6 +843,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                     atomicAdd(&S.start[(uint32_t)((to_ord<DT>(v[q]) - mn) >> shift)], 1u);
         }
         __syncthreads();
+        BG_PROF(1);
         block_exscan(S.start, BIG_DIGITS, S.tmp);
         for (int d = tid; d < BIG_DIGITS; d += bd) S.end[d] = S.start[d];
         __syncthreads();
@@ -797,6 +859,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                 }
         }
         __syncthreads();  // S.end[d] = end of piece d; Y holds the pieces
+        BG_PROF(2);
         if (shift == 0) {  // every piece holds a single value: Y is sorted
             if (Y != Aout)
                 for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = Y[i];
@@ -847,18 +910,34 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                 __syncthreads();
                 for (uint32_t d = dlo + tid; d <= dhi; d += bd) {  // one thread per tiny piece
                     const uint32_t pc = S.end[d] - S.start[d];
-                    if (pc >= 2 && pc <= 16) insertion_sort<DT>(S.sk + (S.start[d] - slo), (int)pc);
+                    if (pc >= 2 && pc <= 8) insertion_sort<DT>(S.sk + (S.start[d] - slo), (int)pc);
                 }
                 for (uint32_t d = dlo + warp; d <= dhi; d += nwarps) {  // one warp per larger piece
                     const uint32_t pc = S.end[d] - S.start[d];
-                    if (pc > 16 && pc <= BIG_CHUNK)
-                        bitonic<DT, false>(S.sk + (S.start[d] - slo), (int)pc, lane, 32);
+                    if ((a.dbg & 512u) && lane == 0 && pc > 1)
+                        atomicAdd(&a.ctl->prof[pc <= 8 ? 6 : pc <= 32 ? 7 : pc <= 64 ? 8 : pc <= 256 ? 9 : pc <= 1024 ? 10 : 11], 1ull);
+                    if (pc <= 8) continue;
+                    uint64_t *g = S.sk + (S.start[d] - slo);
+                    if (pc <= 32) {  // register bitonic across the warp
+                        uint64_t v = (uint32_t)lane < pc ? to_ord<DT>(g[lane]) : ~0ull;
+                        warp_sort32(v, lane);
+                        if ((uint32_t)lane < pc) g[lane] = from_ord<DT>(v);
+                    } else if (pc <= 64) {
+                        warp_sort_piece<DT, 2>(g, pc, lane);
+                    } else if (pc <= 128) {
+                        warp_sort_piece<DT, 4>(g, pc, lane);
+                    } else if (pc <= 256) {
+                        warp_sort_piece<DT, 8>(g, pc, lane);
+                    } else if (pc <= BIG_CHUNK) {
+                        bitonic<DT, false>(g, (int)pc, lane, 32);
+                    }
                 }
                 __syncthreads();
                 for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = S.sk[i];
                 __syncthreads();
             }
         }
+        BG_PROF(3);
         const uint32_t nblk = min(S.nblk, (uint32_t)BIG_MAXBLK);
         for (uint32_t k = 0; k < nblk; k++) {
             const uint32_t d = S.blk[k];
@@ -869,6 +948,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
             for (uint32_t i = tid; i < pc; i += bd) Aout[ps + i] = S.sk[i];
             __syncthreads();
         }
+        BG_PROF(4);
     }
 }
 
