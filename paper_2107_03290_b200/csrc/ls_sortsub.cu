@@ -157,7 +157,7 @@ struct BsSmem {
     uint32_t big[BS_MAXBIG];                // slots of collision groups > 8 keys
     uint32_t wsum[33];
     uint32_t nbig, ovf;
-    uint4 desc[2];                          // {g0, g1, lo, hi} of the window in each slot
+    uint4 dq[4];                            // {g0, g1, lo, hi} of windows it .. it+3 (it & 3)
     unsigned long long st_small, st_smallk, st_h1, st_h1k, st_maxg;
     uint64_t mbar[2];
 };
@@ -188,11 +188,9 @@ __device__ __forceinline__ void bs_issue(BsSmem &S, int slot, const uint64_t *A,
                  &S.mbar[slot]);
 }
 
-// Stage window descriptor d into `slot` (thread 0); the end of the CTA's
-// window sequence is signalled with desc.x = ~0 and an empty transaction so
-// the wait completes.
+// Stage window d into `slot` (thread 0); the end of the CTA's window sequence
+// (d.x = ~0) is an empty transaction so the wait completes.
 __device__ __forceinline__ void bs_stage(BsSmem &S, int slot, const Args &a, uint4 d) {
-    S.desc[slot] = d;
     if (d.x != BS_NONE) bs_issue(S, slot, a.A, d.z, d.w, a.n);
     else mbar_expect_tx(&S.mbar[slot], 0u);
 }
@@ -297,6 +295,23 @@ __device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int la
     }
 }
 
+// Sort c <= 32*NS ord values of a padded-T range by one warp in registers.
+template <int NS>
+__device__ __forceinline__ void warp_sort_T(PadT g, uint32_t c, int lane) {
+    uint64_t v[NS];
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        v[s2] = i < c ? g[i] : ~0ull;
+    }
+    warp_sort_regs<NS>(v, lane);
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        if (i < c) g[i] = v[s2];
+    }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args a) {
     if (a.ctl->status) return;
@@ -308,8 +323,10 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         mbar_init(&S.mbar[0], 1);
         mbar_init(&S.mbar[1], 1);
         S.st_small = S.st_smallk = S.st_h1 = S.st_h1k = S.st_maxg = 0;
-        bs_stage(S, 0, a, bs_desc(a, nwin, 0));
-        bs_stage(S, 1, a, bs_desc(a, nwin, 1));
+        S.dq[0] = bs_desc(a, nwin, 0);
+        S.dq[1] = bs_desc(a, nwin, 1);
+        bs_stage(S, 0, a, S.dq[0]);
+        bs_stage(S, 1, a, S.dq[1]);
     }
     __syncthreads();
     const double rcpF2 = a.rcpF2;
@@ -331,7 +348,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
     for (uint32_t it = 0;; it++) {
         const int slot = (int)(it & 1u);
         // ---- window tables (overlap with the bulk copy in flight)
-        const uint4 desc = S.desc[slot];
+        const uint4 desc = S.dq[it & 3u];
         if (desc.x == BS_NONE) break;
         const uint32_t g0 = desc.x, g1 = desc.y, lo = desc.z, hi = desc.w;
         const int span = (int)(hi - lo);
@@ -350,7 +367,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
             my_st = nx_st;
         }
         {
-            const uint4 nd = S.desc[slot ^ 1];
+            const uint4 nd = S.dq[(it + 1) & 3u];
             nx_np = 0;
             nx_st = 0;
             if (nd.x != BS_NONE && nd.x + tid <= nd.y) {
@@ -425,6 +442,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 code[k] = sl | (r << BS_LOG_W);
             }
         }
+        if (tid == 0) S.dq[(it + 2) & 3u] = ahead;  // read by all at the top of it + 1
         __syncthreads();
         BS_PROF(3);
         // running totals, exclusive (R4): 8 consecutive entries per
@@ -580,12 +598,11 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                     warp_sort32(v, lane);
                     if ((uint32_t)lane < c) T[base + lane] = v;
                 } else if (c <= 64u) {
-                    uint64_t v[2];
-                    v[0] = T[base + lane];
-                    v[1] = (uint32_t)lane + 32u < c ? T[base + 32 + lane] : ~0ull;
-                    warp_sort64(v, lane);
-                    T[base + lane] = v[0];
-                    if ((uint32_t)lane + 32u < c) T[base + 32 + lane] = v[1];
+                    warp_sort_T<2>(T + base, c, lane);
+                } else if (c <= 128u) {
+                    warp_sort_T<4>(T + base, c, lane);
+                } else if (c <= 256u) {
+                    warp_sort_T<8>(T + base, c, lane);
                 } else {
                     bitonic_view(T + base, (int)c, lane, 32);
                 }
