@@ -40,7 +40,8 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        lb1, offs1, hist1, start1, tfirst, tlast, wlist, big, chunks, hist1_u64, B;
+        lb1, offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B;
+    uint32_t task_cap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
@@ -93,6 +94,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
     l.wlist = take((size_t)l.ntiles * 16);
+    l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
+    l.tasks = take((size_t)l.task_cap * 16);
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
@@ -142,6 +145,8 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.tile_first = (uint32_t *)(w + l.tfirst);
     a.tile_last = (uint32_t *)(w + l.tlast);
     a.wlist = (uint4 *)(w + l.wlist);
+    a.tasks = (uint4 *)(w + l.tasks);
+    a.task_cap = l.task_cap;
     a.big = (BigItem *)(w + l.big);
     a.chunks = (BigChunk *)(w + l.chunks);
     a.chunk_cap = l.chunk_cap;

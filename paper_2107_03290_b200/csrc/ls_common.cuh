@@ -179,6 +179,7 @@ enum {
 };
 enum { STATUS_NAN = 1u, STATUS_INTERNAL = 2u };
 constexpr int BIG_LEVELS = 6;
+constexpr uint32_t WS_MAX = 256;  // SMALL sub-buckets up to this size: one warp each (k_warpsort)
 
 struct Ctl {
     uint32_t status;
@@ -187,6 +188,7 @@ struct Ctl {
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
     uint32_t nchunks;                  // k_big_minmax work entries
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
+    uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
     unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
@@ -237,6 +239,8 @@ struct Args {
     uint32_t *start1;                 // [f*f]
     uint32_t *tile_first, *tile_last; // [ntiles]
     uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
+    uint4 *tasks;                     // [task_cap] warp sub-bucket sorts {start, n', g, 0}
+    uint32_t task_cap;
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]
     uint32_t chunk_cap;

@@ -28,6 +28,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
+        ctl->ntask = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
         ctl->smin = ~0ull;
         ctl->smax = 0;
@@ -347,17 +348,46 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     __syncthreads();
     const uint32_t total = block_exscan(s, f, tmp);
     if (tid == 0 && total != nb) atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-    for (int j = tid; j < f; j += blockDim.x) {
-        const uint64_t g = row + j;
-        const uint32_t c = a.hist1[g];
-        const uint32_t st = (uint32_t)bbeg + s[j];
+    // one sub-bucket per thread (f <= 1024 = blockDim.x)
+    const int j = tid;
+    const uint64_t g = row + (uint64_t)(j < f ? j : 0);
+    const uint32_t c = j < f ? a.hist1[g] : 0u;
+    const uint32_t st = j < f ? (uint32_t)bbeg + s[j] : 0u;
+    // SMALL sub-buckets of <= WS_MAX keys become warp tasks (compacted per
+    // block: one global atomic per level-0 bucket)
+    const bool task = j < f && c >= 2u && c <= a.T_small && c <= WS_MAX;
+    {
+        __shared__ uint32_t wcnt[32], wbase;
+        const uint32_t m = __ballot_sync(0xffffffffu, task);
+        const int lane = tid & 31, w = tid >> 5;
+        if (lane == 0) wcnt[w] = __popc(m);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t tot = 0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
+                const uint32_t t = wcnt[q];
+                wcnt[q] = tot;
+                tot += t;
+            }
+            wbase = tot ? atomicAdd(&a.ctl->ntask, tot) : 0u;
+        }
+        __syncthreads();
+        if (task) {
+            const uint32_t k = wbase + wcnt[w] + __popc(m & ((1u << lane) - 1u));
+            if (k < a.task_cap) a.tasks[k] = make_uint4(st, c, (uint32_t)g, 0u);
+            else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+        }
+    }
+    if (j < f) {
         a.start1[g] = st;
         if (c <= 1) {
             if (a.dH1) a.dH1[g] = 1;
         } else if (c <= a.T_small) {
-            const uint32_t t = st / a.T_tile;
-            atomicMin(&a.tile_first[t], (uint32_t)g);
-            atomicMax(&a.tile_last[t], (uint32_t)g);
+            if (!task) {  // middle class: block windows
+                const uint32_t t = st / a.T_tile;
+                atomicMin(&a.tile_first[t], (uint32_t)g);
+                atomicMax(&a.tile_last[t], (uint32_t)g);
+            }
         } else {
             const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
             if (k < a.big_cap) {

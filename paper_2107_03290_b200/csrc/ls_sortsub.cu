@@ -433,7 +433,9 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 uint32_t sl = (uint32_t)i;
                 // (keys of a homogeneous level-0 bucket lying inside the span
                 // have no head of their own: they stay where they are)
-                if (np >= 2u && (uint32_t)i - h < np) {
+                // (sub-buckets of <= WS_MAX keys are sorted by k_warpsort and
+                // stay in place here, like single keys)
+                if (np > WS_MAX && (uint32_t)i - h < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
                     sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         for (uint32_t g = g0 + tid; g <= g1; g += BS_THREADS) {
             const bool first = g == g0 + tid;
             const uint32_t np = first ? my_np : __ldg(&a.hist1[g]);
-            if (np < 2) continue;
+            if (np <= WS_MAX) continue;  // k_warpsort's
             const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
             if (T[h] != T[h + np - 1u]) {  // sorted: homogeneous iff first == last
                 r_small++;
@@ -654,6 +656,231 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         if (S.st_h1) atomicAdd(&a.ctl->stat[ST_H1S], S.st_h1);
         if (S.st_h1k) atomicAdd(&a.ctl->stat[ST_H1K], S.st_h1k);
         if (S.st_maxg) atomicMax(&a.ctl->stat[ST_MAXGRP], S.st_maxg);
+    }
+}
+
+// ------------------------------------------------------ warp sub-bucket sort --
+// One warp per SMALL sub-bucket of 2 <= n' <= WS_MAX keys (k_classify's task
+// list; at 200M keys from smooth distributions that is every sub-bucket). A
+// warp needs no block barrier: the sub-bucket's g, n' and adj are uniform, its
+// keys are loaded coalesced (8 per lane), and Alg. 2's counting sort (P:184-209,
+// pos by R5, exclusive totals R4) and the collision-group touch-up (R15:
+// odd-even transposition between equal-slot neighbours, warp bitonic for
+// groups > 8) run in the warp's own shared-memory slice. A homogeneous
+// sub-bucket (first == last after sorting) is not written back.
+constexpr int WS_WARPS = 8;                 // warps per CTA
+constexpr int WS_KPL = (int)WS_MAX / 32;    // keys per lane (8)
+constexpr int WS_CTAS_PER_SM = 4;
+
+struct WsSlice {
+    uint64_t T[WS_MAX + WS_MAX / 8];        // padded: position q at q + q/8
+    uint32_t K[WS_MAX + 8];                 // pos histogram -> exclusive totals
+    uint16_t slot_of[WS_MAX];
+    uint32_t big[32];                       // groups > 8 keys (their pos)
+};
+
+template <int DT>
+__global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args a) {
+    if (a.ctl->status) return;
+    __shared__ WsSlice SL[WS_WARPS];
+    __shared__ unsigned long long st_red[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WsSlice &W = SL[warp];
+    const PadT T{W.T, 0u};
+    if (threadIdx.x < 4) st_red[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t ntask = min(a.ctl->ntask, a.task_cap);
+    const Root R = load_root(a.M);
+    const uint32_t nw = gridDim.x * WS_WARPS;
+    uint32_t r_small = 0, r_smallk = 0, r_h1 = 0, r_h1k = 0, r_maxg = 0;
+    uint4 nxt = blockIdx.x * WS_WARPS + warp < ntask ? a.tasks[blockIdx.x * WS_WARPS + warp]
+                                                       : make_uint4(0, 0, 0, 0);
+    for (uint32_t t = blockIdx.x * WS_WARPS + warp; t < ntask; t += nw) {
+        const uint4 task = nxt;
+        const uint32_t st = task.x, np = task.y, g = task.z;
+        // keys (coalesced), and the next task's descriptor, in flight together
+        uint64_t key[WS_KPL];
+#pragma unroll
+        for (int k = 0; k < WS_KPL; k++) {
+            const uint32_t i = 32u * k + lane;
+            key[k] = i < np ? a.A[st + i] : 0ull;
+        }
+        if (t + nw < ntask) nxt = a.tasks[t + nw];
+        for (uint32_t i = lane; i <= np; i += 32) W.K[i] = 0;
+        __syncwarp();
+        // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back)
+        const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
+        const double top = (double)(np - 1u);
+        uint32_t code[WS_KPL];
+#pragma unroll
+        for (int k = 0; k < WS_KPL; k++) {
+            const uint32_t i = 32u * k + lane;
+            code[k] = BS_NONE;
+            if (i < np) {
+                const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
+                const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                code[k] = pos | (r << 16);
+            }
+        }
+        __syncwarp();
+        // exclusive running totals over np + 1 <= 257 entries, 9 per lane
+        {
+            constexpr int PER = 9;
+            uint32_t v[PER];
+            uint32_t sum = 0, mg = 0, bigm = 0;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const uint32_t idx = PER * lane + q;
+                const uint32_t c = idx < np ? W.K[idx] : 0u;
+                mg = c > mg ? c : mg;
+                bigm |= (c > BS_RANKMAX ? 1u : 0u) << q;
+                v[q] = sum;
+                sum += c;
+            }
+            const uint32_t incl = warp_incl_scan(sum);
+            const uint32_t off = incl - sum;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const uint32_t idx = PER * lane + q;
+                if (idx <= np) W.K[idx] = v[q] + off;
+            }
+            mg = __reduce_max_sync(0xffffffffu, mg);
+            r_maxg = mg > r_maxg ? mg : r_maxg;
+            // list the groups > 8 (pos values) for the warp sorts below
+            const uint32_t nbl = __popc(bigm);
+            const uint32_t pre = warp_incl_scan(nbl) - nbl;
+            uint32_t m = bigm, o = pre;
+            while (m) {
+                const int q = __ffs(m) - 1;
+                m &= m - 1;
+                if (o < 32) W.big[o] = PER * lane + q;
+                o++;
+            }
+            bigm = __shfl_sync(0xffffffffu, pre + nbl, 31);  // total
+            if (lane == 0) W.K[WS_MAX + 7] = bigm;  // stash the count
+        }
+        __syncwarp();
+        // placement: T[K[pos] + r] = ord(key)
+#pragma unroll
+        for (int k = 0; k < WS_KPL; k++) {
+            if (code[k] != BS_NONE) {
+                const uint32_t pos = code[k] & 0xffffu;
+                const uint32_t q = W.K[pos] + (code[k] >> 16);
+                T[q] = to_ord<DT>(key[k]);
+                W.slot_of[q] = (uint16_t)pos;
+            }
+        }
+        __syncwarp();
+        // touch-up: odd-even transposition between equal-slot neighbours on
+        // 8 consecutive positions per lane (<= 8 rounds, early exit)
+        {
+            const uint32_t q0 = 8u * lane;
+            uint64_t v[8];
+            uint32_t sv[8];
+            {
+                const uint2 s2 = reinterpret_cast<const uint2 *>(W.slot_of)[2 * lane];
+                const uint2 s3 = reinterpret_cast<const uint2 *>(W.slot_of)[2 * lane + 1];
+                const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
+                const uint64_t *row = W.T + 9u * lane;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const bool in = q0 + q < np;
+                    v[q] = in ? row[q] : ~0ull;
+                    sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
+                }
+            }
+            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
+                const bool sw_ = sx == sy && x > y;
+                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
+                x = lo_;
+                y = hi_;
+                return sw_;
+            };
+            for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
+                bool any = false;
+                any |= cx(v[0], v[1], sv[0], sv[1]);
+                any |= cx(v[2], v[3], sv[2], sv[3]);
+                any |= cx(v[4], v[5], sv[4], sv[5]);
+                any |= cx(v[6], v[7], sv[6], sv[7]);
+                any |= cx(v[1], v[2], sv[1], sv[2]);
+                any |= cx(v[3], v[4], sv[3], sv[4]);
+                any |= cx(v[5], v[6], sv[5], sv[6]);
+                const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
+                const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
+                const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
+                const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
+                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                if (!__any_sync(0xffffffffu, any)) break;
+            }
+            if (q0 < np) {
+                uint64_t *row = W.T + 9u * lane;
+#pragma unroll
+                for (int q = 0; q < 8; q++) row[q] = v[q];
+            }
+        }
+        __syncwarp();
+        // groups > 8 keys: register bitonic by the whole warp
+        {
+            const uint32_t nbl = W.K[WS_MAX + 7];
+            for (uint32_t k = 0; k < nbl; k++) {
+                uint32_t pos;
+                if (nbl <= 32) {
+                    pos = W.big[k];
+                } else {  // (more than 32 large groups: rescan the totals)
+                    uint32_t seen = 0;
+                    pos = 0;
+                    for (uint32_t x = 0; x < np; x++)
+                        if (W.K[x + 1] - W.K[x] > BS_RANKMAX && seen++ == k) { pos = x; break; }
+                }
+                const uint32_t base = W.K[pos], c = W.K[pos + 1] - base;
+                bool same = true;
+                for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
+                if (__all_sync(0xffffffffu, same)) continue;
+                if (c <= 32u) {
+                    uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
+                    warp_sort32(v1, lane);
+                    if ((uint32_t)lane < c) T[base + lane] = v1;
+                } else if (c <= 64u) {
+                    warp_sort_T<2>(T + base, c, lane);
+                } else if (c <= 128u) {
+                    warp_sort_T<4>(T + base, c, lane);
+                } else {
+                    warp_sort_T<8>(T + base, c, lane);
+                }
+            }
+        }
+        __syncwarp();
+        // homogeneous iff first == last of the sorted sub-bucket
+        if (T[0] != T[np - 1u]) {
+#pragma unroll
+            for (int k = 0; k < WS_KPL; k++) {
+                const uint32_t i = 32u * k + lane;
+                if (i < np) a.A[st + i] = from_ord<DT>(T[i]);
+            }
+            r_small++;
+            r_smallk += np;
+        } else {
+            if (lane == 0 && a.dH1) a.dH1[g] = 1;
+            r_h1++;
+            r_h1k += np;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (r_small) atomicAdd(&st_red[0], (unsigned long long)r_small);
+        if (r_smallk) atomicAdd(&st_red[1], (unsigned long long)r_smallk);
+        if (r_h1) atomicAdd(&st_red[2], (unsigned long long)r_h1);
+        if (r_h1k) atomicAdd(&st_red[3], (unsigned long long)r_h1k);
+        if (r_maxg > 1) atomicMax(&a.ctl->stat[ST_MAXGRP], (unsigned long long)r_maxg);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (st_red[0]) atomicAdd(&a.ctl->stat[ST_SMALLS], st_red[0]);
+        if (st_red[1]) atomicAdd(&a.ctl->stat[ST_SMALLK], st_red[1]);
+        if (st_red[2]) atomicAdd(&a.ctl->stat[ST_H1S], st_red[2]);
+        if (st_red[3]) atomicAdd(&a.ctl->stat[ST_H1K], st_red[3]);
     }
 }
 
@@ -971,6 +1198,14 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
 
 // -------------------------------------------------------------- launchers --
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int g = sms * WS_CTAS_PER_SM;
+        if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
+        else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
+    }
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
     int dev = 0, sms = 148;
