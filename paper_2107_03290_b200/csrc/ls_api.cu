@@ -40,7 +40,7 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        lb1, offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B;
+        offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B;
     uint32_t task_cap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -81,7 +81,6 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.hist0 = take((size_t)l.f * 8);
     l.bmax0 = take((size_t)l.f * 8);
     l.lb0 = take((size_t)l.U0 * l.f * 8);
-    l.lb1 = take((size_t)l.U1max * l.f * 8);
     l.hist1 = take(ff * 4);
     l.tlast = take((size_t)l.ntiles * 4);
     l.zero_end = off;
@@ -138,7 +137,6 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.unit1_start = (uint32_t *)(w + l.ustart);
     a.lb0 = (unsigned long long *)(w + l.lb0);
     a.offs0 = (uint32_t *)(w + l.offs0);
-    a.lb1 = (unsigned long long *)(w + l.lb1);
     a.offs1 = (uint32_t *)(w + l.offs1);
     a.hist1 = (uint32_t *)(w + l.hist1);
     a.start1 = (uint32_t *)(w + l.start1);
@@ -306,14 +304,14 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     launch_count1(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_COUNT1);
+    launch_classify(a, nullptr, st);  // also turns count1's per-unit counts into offsets
+    launches++;
+    tm.mark(LS_PHASE_CLASSIFY);
     launch_scatter1(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_SCATTER1);
-    launch_classify(a, nullptr, st);
-    launches++;
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
-    tm.mark(LS_PHASE_CLASSIFY);
     launch_bucketsort(a, dt, st);
     launches += 2;
     tm.mark(LS_PHASE_BUCKETSORT);

@@ -233,7 +233,6 @@ struct Args {
     uint32_t *unit1_start;            // [f+1]
     unsigned long long *lb0;          // [U0*f]
     uint32_t *offs0;                  // [U0*f]
-    unsigned long long *lb1;          // [U1max*f]
     uint32_t *offs1;                  // [U1max*f]
     uint32_t *hist1;                  // [f*f]
     uint32_t *start1;                 // [f*f]

@@ -206,6 +206,8 @@ __device__ __forceinline__ int find_bucket(const uint32_t *ustart, int f, uint32
 
 template <int DT>
 __global__ void __launch_bounds__(512) k_count1(Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *leaf = reinterpret_cast<double *>(smem_raw);  // the model's leaves (5 L doubles)
     __shared__ uint32_t hist[LS_MAX_FANOUT];
     __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
     __shared__ unsigned long long s_mn[32], s_mx[32];
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     if (tid == 0) s_unit = atomicAdd(&a.ctl->ticket1, 1u);
     for (int b = tid; b <= f; b += bd) ustart[b] = a.unit1_start[b];
     for (int b = tid; b < f; b += bd) hist[b] = 0;
+    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
     __syncthreads();
     const uint32_t u = s_unit;
     if (u >= a.ctl->U1 || a.ctl->status) return;
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
         const unsigned long long o = to_ord<DT>(key);
         mn = o < mn ? o : mn;
         mx = o > mx ? o : mx;
-        const double p = predict_ldg<DT>(key, R, a.M->leaf);
+        const double p = predict<DT>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
         atomicAdd(&hist[bucket1(p, a.F2, f, (uint32_t)b)], 1u);
     };
     {
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     for (int j = tid; j < f; j += bd) {
         const uint32_t c = hist[j];
         if (c) atomicAdd(&a.hist1[(uint64_t)b * f + j], c);
-        a.offs1[(uint64_t)u * f + j] = lookback(a.lb1, u, ustart[b], f, j, c);
+        a.offs1[(uint64_t)u * f + j] = c;  // per-unit counts; k_classify scans them per bucket
     }
 }
 
@@ -379,6 +382,15 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         }
     }
     if (j < f) {
+        // offs1: per-unit counts (k_count1) -> this unit's offset inside sub-bucket j
+        const uint32_t u0 = a.unit1_start[b], u1 = a.unit1_start[b + 1];
+        uint32_t run = 0;
+        for (uint32_t u = u0; u < u1; u++) {
+            uint32_t *o = &a.offs1[(uint64_t)u * f + j];
+            const uint32_t cnt = *o;
+            *o = run;
+            run += cnt;
+        }
         a.start1[g] = st;
         if (c <= 1) {
             if (a.dH1) a.dH1[g] = 1;
@@ -456,8 +468,9 @@ void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
     else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<a.U0, TP_THREADS, sm, st>>>(a); }
 }
 void launch_count1(const Args &a, int dtype, cudaStream_t st) {
-    if (dtype == DT_F64) k_count1<DT_F64><<<a.U1max, 512, 0, st>>>(a);
-    else k_count1<DT_U64><<<a.U1max, 512, 0, st>>>(a);
+    const size_t sm = (size_t)5 * a.L * sizeof(double);
+    if (dtype == DT_F64) { set_smem(k_count1<DT_F64>, sm); k_count1<DT_F64><<<a.U1max, 512, sm, st>>>(a); }
+    else { set_smem(k_count1<DT_U64>, sm); k_count1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
 }
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(Scatter1Smem);
