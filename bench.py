@@ -170,7 +170,7 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
 
-    multi = world > 1
+    multi = world > 1 or args.force_multi
     wl = args.workload or ("c5_mix" if multi else "c2_normal")
     dist_name, seed = datagen.WORKLOADS[wl]
     if wl == "c5_mix":
@@ -184,7 +184,7 @@ def run_ours(args):
     cfg = ls.config(flags=ls.LS_FLAG_PHASE_TIMING)
     dt = ls.dtype_code(pristine)
     if multi:
-        comm = ls.Comm.from_torch_distributed()
+        comm = ls.Comm.from_torch_distributed() if world > 1 else ls.Comm(0, 1, ls.Comm.unique_id())
         out_cap = int(n * 1.25) + 1_000_000
         out = torch.empty(out_cap, dtype=tdt, device=dev)
         ws = torch.empty(ls.multi_workspace_bytes(n, out_cap, world, dt, cfg), dtype=torch.uint8,
@@ -209,13 +209,13 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         one_step()
-    if multi:
+    if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     times, stats = [], []
     with ClockSampler(local) as clk:
         clk.wait_first()
-        if multi:
+        if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         clk.mark("t_start")
@@ -225,10 +225,10 @@ def run_ours(args):
             stats.append(st)
         torch.cuda.synchronize()
         clk.mark("t_end")
-        if multi:
+        if world > 1:
             dist.barrier()
     total_ms = sum(times)
-    if multi:
+    if world > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -311,6 +311,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if multi:
         comm.close()
+    if world > 1:
         dist.destroy_process_group()
 
 
@@ -411,6 +412,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=10_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-multi", action="store_true",
+                    help="run the ls_sort_multi path (config 5) even at world size 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 is below the contract minimum", file=sys.stderr)
