@@ -40,8 +40,9 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B;
-    uint32_t task_cap;
+        offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
+        lstart, lcur, lhom, lmin, lmax, pieces;
+    uint32_t task_cap, lcap, pcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
@@ -73,6 +74,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     };
     l.ff_begin = align_up(off, 256);
     l.leaf_min = take((size_t)l.L * 8);
+    l.lcap = (uint32_t)(n / (LARGE_MIN + 1) + 1);
+    l.lmin = take((size_t)l.lcap * 1024 * 8);
     l.bmin0 = take((size_t)l.f * 8);
     l.tfirst = take((size_t)l.ntiles * 4);
     l.ff_end = off;
@@ -83,6 +86,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.lb0 = take((size_t)l.U0 * l.f * 8);
     l.hist1 = take(ff * 4);
     l.tlast = take((size_t)l.ntiles * 4);
+    l.ltot = take((size_t)l.lcap * 1024 * 4);
+    l.lmax = take((size_t)l.lcap * 1024 * 8);
     l.zero_end = off;
     l.ctl = take(sizeof(Ctl));
     l.model = take(sizeof(DevModel));
@@ -95,6 +100,12 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.wlist = take((size_t)l.ntiles * 16);
     l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
     l.tasks = take((size_t)l.task_cap * 16);
+    l.large = take((size_t)l.lcap * 4);
+    l.lstart = take((size_t)l.lcap * 1024 * 4);
+    l.lcur = take((size_t)l.lcap * 1024 * 4);
+    l.lhom = take((size_t)l.lcap * 32 * 4);
+    l.pcap = (uint32_t)(n / 4 + 64);
+    l.pieces = take((size_t)l.pcap * 8);
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
@@ -144,6 +155,16 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.tile_last = (uint32_t *)(w + l.tlast);
     a.wlist = (uint4 *)(w + l.wlist);
     a.tasks = (uint4 *)(w + l.tasks);
+    a.large = (uint32_t *)(w + l.large);
+    a.lcap = l.lcap;
+    a.pcap = l.pcap;
+    a.ltot = (uint32_t *)(w + l.ltot);
+    a.lstart = (uint32_t *)(w + l.lstart);
+    a.lcur = (uint32_t *)(w + l.lcur);
+    a.lhom = (uint32_t *)(w + l.lhom);
+    a.lmin = (unsigned long long *)(w + l.lmin);
+    a.lmax = (unsigned long long *)(w + l.lmax);
+    a.pieces = (uint2 *)(w + l.pieces);
     a.task_cap = l.task_cap;
     a.big = (BigItem *)(w + l.big);
     a.chunks = (BigChunk *)(w + l.chunks);
@@ -317,6 +338,8 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     tm.mark(LS_PHASE_BUCKETSORT);
     launch_big_minmax(a, dt, st);
     launches++;
+    launch_large(a, dt, st);
+    launches += 5;
     for (int lv = 0; lv < BIG_LEVELS; lv++) {
         launch_big(a, lv, dt, st);
         launches++;

@@ -180,6 +180,7 @@ enum {
 enum { STATUS_NAN = 1u, STATUS_INTERNAL = 2u };
 constexpr int BIG_LEVELS = 6;
 constexpr uint32_t WS_MAX = 256;  // SMALL sub-buckets up to this size: one warp each (k_warpsort)
+constexpr uint32_t LARGE_MIN = 262144;  // big sub-buckets above this: grid-parallel path (ls_bigpath.cu)
 
 struct Ctl {
     uint32_t status;
@@ -189,6 +190,7 @@ struct Ctl {
     uint32_t nchunks;                  // k_big_minmax work entries
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
+    uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
     unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
@@ -240,6 +242,12 @@ struct Args {
     uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
     uint4 *tasks;                     // [task_cap] warp sub-bucket sorts {start, n', g, 0}
     uint32_t task_cap;
+    // large big items (> LARGE_MIN keys): per item 1024-digit tables
+    uint32_t *large;                  // [lcap] index into big[] (level 0)
+    uint32_t lcap, pcap;
+    uint32_t *ltot, *lstart, *lcur, *lhom;  // [lcap*1024] x3, [lcap*32]
+    unsigned long long *lmin, *lmax;  // [lcap*1024]
+    uint2 *pieces;                    // [pcap] small non-homogeneous pieces {off, size} (in B)
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]
     uint32_t chunk_cap;

@@ -30,6 +30,7 @@ void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st);
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);
 void launch_big(const Args &a, int level, int dtype, cudaStream_t st);
+void launch_large(const Args &a, int dtype, cudaStream_t st);  // ls_bigpath.cu
 
 // parity hooks (ls_partition.cu)
 void launch_bucket_ids(const uint64_t *keys, uint64_t n, int f, const DevModel *M, double *p,

@@ -29,6 +29,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = 0;
+        ctl->nlarge = ctl->npiece = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
         ctl->smin = ~0ull;
         ctl->smax = 0;
@@ -403,7 +404,17 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         } else {
             const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
             if (k < a.big_cap) {
-                a.big[k] = BigItem{st, c, 0u, (uint32_t)g, ~0ull, 0ull, 0u, 0u};
+                uint32_t lrk = 0;  // large items: grid-parallel path (ls_bigpath.cu)
+                if (c > LARGE_MIN) {
+                    const uint32_t li = atomicAdd(&a.ctl->nlarge, 1u);
+                    if (li < a.lcap) {
+                        a.large[li] = k;
+                        lrk = li + 1u;
+                    } else {
+                        atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+                    }
+                }
+                a.big[k] = BigItem{st, c, 0u, (uint32_t)g, ~0ull, 0ull, lrk, 0u};
                 const uint32_t nch = (c + MM_CHUNK - 1) / MM_CHUNK;
                 const uint32_t base = atomicAdd(&a.ctl->nchunks, nch);
                 for (uint32_t q = 0; q < nch; q++)

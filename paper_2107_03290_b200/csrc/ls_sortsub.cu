@@ -14,6 +14,7 @@
 // range) into the scratch copy, then every piece is sorted in shared memory;
 // pieces larger than the shared-memory sort capacity go to the next level.
 #include "ls_launch.h"
+#include "ls_warpsort.cuh"
 
 namespace ls {
 
@@ -208,91 +209,6 @@ __device__ __forceinline__ double adj_of(uint32_t g, double F2, double rcp) {
     const double gd = (double)g;
     const double q0 = __dmul_rn(gd, rcp);
     return __fma_rn(__fma_rn(-q0, F2, gd), rcp, q0);
-}
-
-// Ascending bitonic sort of 32 (one per lane) or 64 (two per lane, element
-// lane + 32 s in v[s]) ord values across a warp, in registers.
-__device__ __forceinline__ void warp_sort32(uint64_t &v, int lane) {
-#pragma unroll
-    for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            const uint64_t w = __shfl_xor_sync(0xffffffffu, v, jj);
-            const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
-            v = keep_min ? (w < v ? w : v) : (w > v ? w : v);
-        }
-    }
-}
-__device__ __forceinline__ void warp_sort64(uint64_t v[2], int lane) {
-#pragma unroll
-    for (int kk = 2; kk <= 64; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            if (jj == 32) {  // partner in the other register of the same lane (kk == 64: ascending)
-                const uint64_t lo_ = v[0] < v[1] ? v[0] : v[1], hi_ = v[0] < v[1] ? v[1] : v[0];
-                v[0] = lo_;
-                v[1] = hi_;
-            } else {
-#pragma unroll
-                for (int s2 = 0; s2 < 2; s2++) {
-                    const int i = lane + 32 * s2;
-                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
-                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
-                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
-                }
-            }
-        }
-    }
-}
-
-// Ascending bitonic sort of 32*NS ord values across a warp, in registers:
-// element i = 32*s + lane lives in v[s]. Partners at distance >= 32 are in the
-// same lane (register compare-exchange), closer ones are one shuffle away.
-template <int NS>
-__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[NS], int lane) {
-#pragma unroll
-    for (int kk = 2; kk <= 32 * NS; kk <<= 1) {
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-            if (jj >= 32) {
-                const int js = jj >> 5;
-#pragma unroll
-                for (int s2 = 0; s2 < NS; s2++) {
-                    if (s2 & js) continue;
-                    const int i = 32 * s2 + lane;
-                    const bool asc = (i & kk) == 0;
-                    const uint64_t x = v[s2], y = v[s2 | js];
-                    const bool sw_ = asc ? (x > y) : (x < y);
-                    v[s2] = sw_ ? y : x;
-                    v[s2 | js] = sw_ ? x : y;
-                }
-            } else {
-#pragma unroll
-                for (int s2 = 0; s2 < NS; s2++) {
-                    const int i = 32 * s2 + lane;
-                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
-                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
-                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
-                }
-            }
-        }
-    }
-}
-
-template <int DT, int NS>
-__device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int lane) {
-    uint64_t v[NS];
-#pragma unroll
-    for (int s2 = 0; s2 < NS; s2++) {
-        const uint32_t i = 32u * s2 + lane;
-        v[s2] = i < pc ? to_ord<DT>(g[i]) : ~0ull;
-    }
-    warp_sort_regs<NS>(v, lane);
-#pragma unroll
-    for (int s2 = 0; s2 < NS; s2++) {
-        const uint32_t i = 32u * s2 + lane;
-        if (i < pc) g[i] = from_ord<DT>(v[s2]);
-    }
 }
 
 // Sort c <= 32*NS ord values of a padded-T range by one warp in registers.
@@ -1060,6 +976,10 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                 atomicAdd(&a.ctl->stat[ST_BIGK], (unsigned long long)item.size);
             }
             atomicAdd(&a.ctl->stat[ST_BIGPASS], 1ull);
+        }
+        if (level == 0 && item.pad0) {  // large: sorted by ls_bigpath.cu
+            __syncthreads();
+            continue;
         }
         if (item.size <= BIG_SORT_CAP) {
             for (uint32_t i = tid; i < item.size; i += bd) S.sk[i] = X[i];

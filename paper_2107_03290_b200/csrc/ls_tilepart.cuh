@@ -35,8 +35,11 @@ struct TpSmem {
     uint32_t ex[LS_MAX_FANOUT];
     uint32_t delta[LS_MAX_FANOUT];
     uint32_t wsum[33];
+    uint32_t tot;
     uint64_t mbar[2];
 };
+
+constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (SKIP mode)
 
 // Issue the bulk copy of src[t0, t1) into ring slot `slot`, so that key k lands
 // at slot[k - (t0 & ~1)]. The bulk engine moves 16-byte-aligned ranges, so the
@@ -65,7 +68,7 @@ __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *sr
 // base[] is in shared memory, owned by thread b. bf(key, index) -> bucket.
 // All threads of the CTA call it; S.mbar must have been initialised (count 1)
 // by tp_init and every phase used so far is tracked in `phase`.
-template <class BF>
+template <bool SKIP = false, class BF>
 __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
@@ -94,8 +97,10 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             if (idx < tn) {
                 key[k] = keys[idx];
                 const uint32_t b = bf(key[k], t0 + idx);
-                const uint32_t r = atomicAdd(&S.cnt[b], 1u);
-                code[k] = b | (r << 10);
+                if (!SKIP || b != TP_SKIP) {
+                    const uint32_t r = atomicAdd(&S.cnt[b], 1u);
+                    code[k] = b | (r << 10);
+                }
             }
         }
         __syncthreads();
@@ -108,6 +113,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             const uint32_t v = S.wsum[lane];
             const uint32_t vi = warp_incl_scan(v);
             S.wsum[lane] = vi - v;
+            if (SKIP && lane == 31) S.tot = vi;  // keys that move in this tile
         }
         __syncthreads();
         if (tid < nb) {
@@ -134,12 +140,13 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         }
         __syncthreads();
         {
+            const int tm = SKIP ? (int)S.tot : tn;
             uint32_t b[TP_KPT], d[TP_KPT];
             uint64_t v[TP_KPT];
 #pragma unroll
             for (int k = 0; k < TP_KPT; k++) {
                 const int idx = k * TP_THREADS + tid;
-                b[k] = idx < tn ? S.sbin[idx] : 0u;
+                b[k] = idx < tm ? S.sbin[idx] : 0u;
                 v[k] = sk[idx];
             }
 #pragma unroll
@@ -147,7 +154,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
 #pragma unroll
             for (int k = 0; k < TP_KPT; k++) {
                 const int idx = k * TP_THREADS + tid;
-                if (idx < tn) dst[d[k] + (uint32_t)idx] = v[k];
+                if (idx < tm) dst[d[k] + (uint32_t)idx] = v[k];
             }
         }
         __syncthreads();

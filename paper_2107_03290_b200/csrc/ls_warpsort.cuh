@@ -1,0 +1,93 @@
+// ls_warpsort.cuh -- warp-wide sorting networks in registers (shuffles), used
+// for collision groups (ls_sortsub.cu) and big-path pieces (ls_bigpath.cu).
+#pragma once
+#include "ls_common.cuh"
+
+namespace ls {
+
+// Ascending bitonic sort of 32 (one per lane) or 64 (two per lane, element
+// lane + 32 s in v[s]) ord values across a warp, in registers.
+__device__ __forceinline__ void warp_sort32(uint64_t &v, int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            const uint64_t w = __shfl_xor_sync(0xffffffffu, v, jj);
+            const bool keep_min = ((lane & jj) == 0) == ((lane & kk) == 0);
+            v = keep_min ? (w < v ? w : v) : (w > v ? w : v);
+        }
+    }
+}
+__device__ __forceinline__ void warp_sort64(uint64_t v[2], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj == 32) {  // partner in the other register of the same lane (kk == 64: ascending)
+                const uint64_t lo_ = v[0] < v[1] ? v[0] : v[1], hi_ = v[0] < v[1] ? v[1] : v[0];
+                v[0] = lo_;
+                v[1] = hi_;
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < 2; s2++) {
+                    const int i = lane + 32 * s2;
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
+                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
+                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
+                }
+            }
+        }
+    }
+}
+
+// Ascending bitonic sort of 32*NS ord values across a warp, in registers:
+// element i = 32*s + lane lives in v[s]. Partners at distance >= 32 are in the
+// same lane (register compare-exchange), closer ones are one shuffle away.
+template <int NS>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[NS], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32 * NS; kk <<= 1) {
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            if (jj >= 32) {
+                const int js = jj >> 5;
+#pragma unroll
+                for (int s2 = 0; s2 < NS; s2++) {
+                    if (s2 & js) continue;
+                    const int i = 32 * s2 + lane;
+                    const bool asc = (i & kk) == 0;
+                    const uint64_t x = v[s2], y = v[s2 | js];
+                    const bool sw_ = asc ? (x > y) : (x < y);
+                    v[s2] = sw_ ? y : x;
+                    v[s2 | js] = sw_ ? x : y;
+                }
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < NS; s2++) {
+                    const int i = 32 * s2 + lane;
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, v[s2], jj);
+                    const bool keep_min = ((i & jj) == 0) == ((i & kk) == 0);
+                    v[s2] = keep_min ? (w < v[s2] ? w : v[s2]) : (w > v[s2] ? w : v[s2]);
+                }
+            }
+        }
+    }
+}
+
+template <int DT, int NS>
+__device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int lane) {
+    uint64_t v[NS];
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        v[s2] = i < pc ? to_ord<DT>(g[i]) : ~0ull;
+    }
+    warp_sort_regs<NS>(v, lane);
+#pragma unroll
+    for (int s2 = 0; s2 < NS; s2++) {
+        const uint32_t i = 32u * s2 + lane;
+        if (i < pc) g[i] = from_ord<DT>(v[s2]);
+    }
+}
+
+}  // namespace ls

@@ -328,3 +328,43 @@ def test_sort_multi_single_rank():
         assert e.value.status == ls.LS_E_CAPACITY
     finally:
         comm.close()
+
+
+# -------------------------------------------------- large big sub-buckets --
+
+def _clusters(dtype, seed):
+    """Three tight clusters of 400K keys each (the model cannot separate them:
+    large BIG sub-buckets) plus a uniform background."""
+    rng = np.random.default_rng(seed)
+    if dtype == np.uint64:
+        parts = [np.uint64(c) + rng.integers(0, 5000, 400_000).astype(np.uint64)
+                 for c in (10 ** 15, 2 ** 62, 2 ** 63 + 12345)]
+        parts.append(rng.integers(0, 2 ** 64 - 1, 200_000, dtype=np.uint64))
+    else:
+        parts = [c + rng.integers(0, 5000, 400_000) * 1e-9 for c in (-3.0, 0.25, 7e3)]
+        parts.append(rng.uniform(-1e4, 1e4, 200_000))
+        parts.append(np.array([np.inf, -np.inf, 0.0] * 100))
+    a = np.concatenate(parts).astype(dtype)
+    rng.shuffle(a)
+    return a
+
+
+@pytest.mark.parametrize("case", ["cfg5mix", "clusters_u64", "clusters_f64", "twovalue"])
+def test_large_big_items(case):
+    """Sub-buckets > 64K keys take the grid-parallel path (ls_bigpath.cu):
+    homogeneous digit pieces filled by value, the rest scattered and sorted."""
+    if case == "cfg5mix":
+        keys = gen("cfg5mix", 6_000_000, 1000)
+    elif case == "twovalue":
+        rng = np.random.default_rng(3)
+        a = np.where(rng.random(2_000_000) < 0.5, 1.0, 2.0)
+        a[:1000] = rng.uniform(0, 1e6, 1000)
+        keys = from_np(a)
+    else:
+        keys = from_np(_clusters(np.uint64 if case.endswith("u64") else np.float64, 7))
+    h = to_np(keys)
+    t = keys.clone()
+    st = ls.ls_sort(t)
+    assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
+    if case.startswith("clusters"):
+        assert st["big_keys"] >= 800_000
