@@ -64,8 +64,9 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.ntiles = (uint32_t)((n + l.T_tile - 1) / l.T_tile);
     if (l.ntiles == 0) l.ntiles = 1;
     const uint64_t ff = (uint64_t)l.f * l.f;
-    l.big_cap = (uint32_t)((n / (l.T_small + 1) + 1) < ff ? (n / (l.T_small + 1) + 1) : ff);
-    if (l.big_cap < 64) l.big_cap = 64;
+    // big items per level: level 0 holds sub-buckets > T_small keys; deeper
+    // levels hold pieces > 256 keys (ls_bigpath.cu) or > BIG_SORT_CAP (k_big)
+    l.big_cap = (uint32_t)(n / 257 + 64);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = align_up(off, 256);
