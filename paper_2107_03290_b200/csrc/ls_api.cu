@@ -41,7 +41,7 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid;
     uint32_t task_cap, lcap, pcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -99,6 +99,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
     l.wlist = take((size_t)l.ntiles * 16);
+    l.bid = take((size_t)(n + 16) * 2);
     l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
     l.tasks = take((size_t)l.task_cap * 16);
     l.large = take((size_t)l.lcap * 4);
@@ -155,6 +156,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.tile_first = (uint32_t *)(w + l.tfirst);
     a.tile_last = (uint32_t *)(w + l.tlast);
     a.wlist = (uint4 *)(w + l.wlist);
+    a.bid = (uint16_t *)(w + l.bid);
     a.tasks = (uint4 *)(w + l.tasks);
     a.large = (uint32_t *)(w + l.large);
     a.lcap = l.lcap;

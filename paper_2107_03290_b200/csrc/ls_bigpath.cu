@@ -152,6 +152,8 @@ struct LargeSmem {
     uint32_t hom[LD_WORDS];
 };
 
+static_assert(sizeof(LargeSmem) <= MAX_SMEM_OPTIN, "large scatter shared memory");
+
 template <int DT>
 __global__ void __launch_bounds__(TP_THREADS, 1) k_large_scatter(Args a) {
     if (a.ctl->status) return;

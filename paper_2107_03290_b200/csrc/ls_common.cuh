@@ -240,6 +240,7 @@ struct Args {
     uint32_t *start1;                 // [f*f]
     uint32_t *tile_first, *tile_last; // [ntiles]
     uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
+    uint16_t *bid;                    // [n + 16] bucket id of each key, count -> scatter pass
     uint4 *tasks;                     // [task_cap] warp sub-bucket sorts {start, n', g, 0}
     uint32_t task_cap;
     // large big items (> LARGE_MIN keys): per item 1024-digit tables

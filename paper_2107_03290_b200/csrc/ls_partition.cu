@@ -165,6 +165,11 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     }
 }
 
+// Bucket ids precomputed by the count pass (tile_partition BIDS mode).
+struct NoBucket {
+    __device__ __forceinline__ uint32_t operator()(uint64_t, uint64_t) const { return 0u; }
+};
+
 // Level-0 bucket through the b0 search tables (shared memory).
 template <int DT>
 struct B0Bucket {
@@ -228,21 +233,25 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     const uint64_t end = umin64(bend, beg + a.C1);
     const Root R = load_root(a.M);
     unsigned long long mn = ~0ull, mx = 0;
-    auto one = [&](uint64_t key) {
+    auto one = [&](uint64_t key) -> uint32_t {
         const unsigned long long o = to_ord<DT>(key);
         mn = o < mn ? o : mn;
         mx = o > mx ? o : mx;
         const double p = predict<DT>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
-        atomicAdd(&hist[bucket1(p, a.F2, f, (uint32_t)b)], 1u);
+        const uint32_t b1 = bucket1(p, a.F2, f, (uint32_t)b);
+        atomicAdd(&hist[b1], 1u);
+        return b1;
     };
     {
-        // 16-byte loads, 4 in flight per thread; odd head / tail keys apart
+        // 16-byte loads, 4 in flight per thread; odd head / tail keys apart.
+        // b1 of every key is kept (2 bytes) for k_scatter1.
         uint64_t i0 = beg;
         if ((i0 & 1) && i0 < end) {
-            if (tid == 0) one(a.B[i0]);
+            if (tid == 0) a.bid[i0] = (uint16_t)one(a.B[i0]);
             i0++;
         }
         const ulonglong2 *B2 = reinterpret_cast<const ulonglong2 *>(a.B + i0);
+        uint32_t *bid2 = reinterpret_cast<uint32_t *>(a.bid + i0);
         const uint64_t np = (end - i0) / 2;
         uint64_t i = tid;
         for (; i + 3 * bd < np; i += 4 * bd) {
@@ -250,17 +259,13 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
 #pragma unroll
             for (int q = 0; q < 4; q++) v[q] = __ldcs(B2 + i + q * bd);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                one(v[q].x);
-                one(v[q].y);
-            }
+            for (int q = 0; q < 4; q++) bid2[i + q * bd] = one(v[q].x) | (one(v[q].y) << 16);
         }
         for (; i < np; i += bd) {
             const ulonglong2 v = __ldcs(B2 + i);
-            one(v.x);
-            one(v.y);
+            bid2[i] = one(v.x) | (one(v.y) << 16);
         }
-        if (((end - i0) & 1) && tid == 0) one(a.B[end - 1]);
+        if (((end - i0) & 1) && tid == 0) a.bid[end - 1] = (uint16_t)one(a.B[end - 1]);
     }
     mn = warp_min_u64(mn);
     mx = warp_max_u64(mx);
@@ -286,9 +291,13 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
 
 struct Scatter1Smem {
     TpSmem tp;
+    alignas(16) TpBids sbid;
     uint32_t base[LS_MAX_FANOUT];
     uint32_t ustart[LS_MAX_FANOUT + 1];
 };
+
+static_assert(sizeof(Scatter0Smem) <= MAX_SMEM_OPTIN, "scatter0 shared memory");
+static_assert(sizeof(Scatter1Smem) <= MAX_SMEM_OPTIN, "scatter1 shared memory");
 
 template <int DT>
 __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
@@ -319,9 +328,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     block_exscan(tst, f, S.tp.wsum);
     for (int j = tid; j < f; j += bd) S.base[j] = (uint32_t)bbeg + tst[j] + a.offs1[(uint64_t)u * f + j];
     tp_init(S.tp);
-    const ModelBucket<DT, 1, false> bf{load_root(a.M), a.M->leaf, a.F, a.F2, f, (uint32_t)b};
     uint32_t phase = 0;
-    tile_partition(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase);
+    const NoBucket bf{};
+    tile_partition<false, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid);
 }
 
 // ------------------------------------------------------------- classify ----

@@ -906,6 +906,8 @@ __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long 
     __syncthreads();
 }
 
+static_assert(sizeof(BsSmem) * BS_CTAS_PER_SM <= 228 * 1024, "bucket sort shared memory per SM");
+
 struct BigSmem {
     uint64_t sk[BIG_SORT_CAP];
     uint32_t start[BIG_DIGITS], end[BIG_DIGITS];

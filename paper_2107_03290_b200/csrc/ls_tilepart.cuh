@@ -28,6 +28,9 @@ constexpr int TP_KPT = 8;
 constexpr int TP_TILE = TP_THREADS * TP_KPT;  // 8192 keys
 constexpr int TP_SLOT = TP_TILE + 2;          // + aligned-hull slack
 
+constexpr size_t MAX_SMEM_OPTIN = 232448;  // 227 KB per block on sm_100
+typedef uint16_t TpBids[2][TP_TILE + 16];  // staged precomputed bucket ids (BIDS mode)
+
 struct TpSmem {
     uint64_t ring[2][TP_SLOT];
     uint16_t sbin[TP_TILE];
@@ -47,7 +50,8 @@ constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (
 // would run past the end of the array (len odd, t1 == len) is the last key
 // loaded by this (single) thread directly.
 __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *src, uint64_t t0,
-                                         uint64_t t1, uint64_t len) {
+                                         uint64_t t1, uint64_t len, const uint16_t *bid = nullptr,
+                                         TpBids *sb = nullptr) {
     uint64_t *dst = S.ring[slot];
     const uint64_t a0 = t0 & ~1ull;
     uint64_t a1 = (t1 + 1) & ~1ull;
@@ -56,11 +60,15 @@ __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *sr
         dst[t1 - 1 - a0] = src[t1 - 1];
     }
     const uint32_t bytes = a1 > a0 ? (uint32_t)((a1 - a0) * 8) : 0u;
-    mbar_expect_tx(&S.mbar[slot], bytes);
+    // bucket ids: 16-byte-aligned hull of [t0, t1) (the id array is padded)
+    const uint64_t s0 = t0 & ~7ull, s1 = (t1 + 7) & ~7ull;
+    const uint32_t sbytes = bid ? (uint32_t)((s1 - s0) * 2) : 0u;
+    mbar_expect_tx(&S.mbar[slot], bytes + sbytes);
     constexpr uint32_t CH = 32768;
     for (uint32_t o = 0; o < bytes; o += CH)
         bulk_g2s((char *)dst + o, (const char *)(src + a0) + o, bytes - o < CH ? bytes - o : CH,
                  &S.mbar[slot]);
+    if (bid) bulk_g2s((*sb)[slot], bid + s0, sbytes, &S.mbar[slot]);
 }
 
 // Partition src[beg, end) into nb <= 1024 buckets: key -> dst[base[b]++].
@@ -68,17 +76,22 @@ __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *sr
 // base[] is in shared memory, owned by thread b. bf(key, index) -> bucket.
 // All threads of the CTA call it; S.mbar must have been initialised (count 1)
 // by tp_init and every phase used so far is tracked in `phase`.
-template <bool SKIP = false, class BF>
+// BIDS: the bucket of key i is bid[i] (precomputed by the count pass, staged
+// by the bulk engine next to the keys); bf is not called.
+template <bool SKIP = false, bool BIDS = false, class BF>
 __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
-                                               int nb, const BF &bf, uint32_t &phase) {
+                                               int nb, const BF &bf, uint32_t &phase,
+                                               const uint16_t *bid = nullptr, TpBids *sb = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
     if (ntl == 0) return;
     if (tid == 0) {
-        tp_issue(S, 0, src, beg, umin64(end, beg + TP_TILE), len);
-        if (ntl > 1) tp_issue(S, 1, src, beg + TP_TILE, umin64(end, beg + 2 * TP_TILE), len);
+        tp_issue(S, 0, src, beg, umin64(end, beg + TP_TILE), len, BIDS ? bid : nullptr, sb);
+        if (ntl > 1)
+            tp_issue(S, 1, src, beg + TP_TILE, umin64(end, beg + 2 * TP_TILE), len, BIDS ? bid : nullptr,
+                     sb);
     }
     if (tid < nb) S.cnt[tid] = 0;
     __syncthreads();
@@ -88,6 +101,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         const int tn = (int)umin64((uint64_t)TP_TILE, end - t0);
         mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
         const uint64_t *keys = S.ring[slot] + (t0 & 1);
+        const uint16_t *bids = BIDS ? (*sb)[slot] + (t0 & 7) : nullptr;
         uint64_t key[TP_KPT];
         uint32_t code[TP_KPT];
 #pragma unroll
@@ -96,7 +110,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             code[k] = 0xffffffffu;
             if (idx < tn) {
                 key[k] = keys[idx];
-                const uint32_t b = bf(key[k], t0 + idx);
+                const uint32_t b = BIDS ? (uint32_t)bids[idx] : bf(key[k], t0 + idx);
                 if (!SKIP || b != TP_SKIP) {
                     const uint32_t r = atomicAdd(&S.cnt[b], 1u);
                     code[k] = b | (r << 10);
@@ -160,7 +174,8 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         __syncthreads();
         phase ^= 1u << slot;
         if (tid == 0 && i + 2 < ntl)
-            tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE), len);
+            tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE), len,
+                     BIDS ? bid : nullptr, sb);
     }
 }
 

@@ -9,7 +9,8 @@ import subprocess
 import sys
 
 PHASE_OF = {"k_count0": "count0", "k_scatter0": "scatter0", "k_count1": "count1",
-            "k_scatter1": "scatter1", "k_bucketsort": "bucketsort", "k_big": "big"}
+            "k_scatter1": "scatter1", "k_warpsort": "bucketsort", "k_bucketsort": "bucketsort",
+            "k_big": "big"}
 
 
 def launches(path, out):
@@ -68,8 +69,9 @@ def full(rep, out, n):
                 x = float(r[i].replace(",", ""))
                 u = units[i]
                 return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-            traffic[ph] = {"n": n, "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
-                           "kernel": name}
+            e = traffic.setdefault(ph, {"n": n, "dram_bytes_per_launch": 0.0, "kernel": ""})
+            e["dram_bytes_per_launch"] += val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+            e["kernel"] = (e["kernel"] + " + " if e["kernel"] else "") + name
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
