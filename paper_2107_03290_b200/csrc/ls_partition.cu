@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
     tp_init(S.tp);
     const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
     uint32_t phase = 0;
-    tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase);
+    tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase, nullptr, nullptr,
+                   (a.dbg & 1024u) ? a.ctl->prof : nullptr);
 }
 
 // --------------------------------------------------------------- round 1 ---
@@ -330,7 +331,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     tp_init(S.tp);
     uint32_t phase = 0;
     const NoBucket bf{};
-    tile_partition<false, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid);
+    tile_partition<false, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid,
+                                (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr);
 }
 
 // ------------------------------------------------------------- classify ----

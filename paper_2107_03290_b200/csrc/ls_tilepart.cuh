@@ -83,7 +83,16 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
                                                int nb, const BF &bf, uint32_t &phase,
-                                               const uint16_t *bid = nullptr, TpBids *sb = nullptr) {
+                                               const uint16_t *bid = nullptr, TpBids *sb = nullptr,
+                                               unsigned long long *prof = nullptr) {
+    long long tq = clock64();
+    auto mark = [&](int k) {
+        if (prof && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(&prof[k], (unsigned long long)(t - tq));
+            tq = t;
+        }
+    };
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
     if (ntl == 0) return;
@@ -100,6 +109,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         const uint64_t t0 = beg + i * TP_TILE;
         const int tn = (int)umin64((uint64_t)TP_TILE, end - t0);
         mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
+        mark(0);
         const uint64_t *keys = S.ring[slot] + (t0 & 1);
         const uint16_t *bids = BIDS ? (*sb)[slot] + (t0 & 7) : nullptr;
         uint64_t key[TP_KPT];
@@ -118,6 +128,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             }
         }
         __syncthreads();
+        mark(1);
         // exclusive scan of the tile's bucket counts; advance the cursors
         uint32_t c = tid < nb ? S.cnt[tid] : 0u;
         const uint32_t incl = warp_incl_scan(c);
@@ -138,6 +149,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             S.cnt[tid] = 0;
         }
         __syncthreads();
+        mark(2);
         // bucket-contiguous order inside the consumed slot (all lookups
         // first, then all stores: independent shared-memory chains)
         uint64_t *sk = S.ring[slot];
@@ -153,6 +165,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             }
         }
         __syncthreads();
+        mark(3);
         {
             const int tm = SKIP ? (int)S.tot : tn;
             uint32_t b[TP_KPT], d[TP_KPT];
@@ -172,6 +185,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
             }
         }
         __syncthreads();
+        mark(4);
         phase ^= 1u << slot;
         if (tid == 0 && i + 2 < ntl)
             tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE), len,
