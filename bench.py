@@ -114,16 +114,17 @@ class ClockSampler:
 
 
 def phase_bytes(phase: str, n: int, st: dict) -> float:
-    """Algorithmic HBM bytes of one launch of a phase, 8-byte keys."""
+    """Algorithmic HBM bytes of one launch of a phase, 8-byte keys.
+    count1 also stores each key's 2-byte b1, which scatter1 reads back."""
     h0 = st["h0_keys"]
     if phase == "count0":
         return 8.0 * n
     if phase == "scatter0":
         return 16.0 * n
     if phase == "count1":
-        return 8.0 * n
+        return 10.0 * (n - h0) + 8.0 * h0
     if phase == "scatter1":
-        return 16.0 * (n - h0) + 8.0 * h0
+        return 18.0 * (n - h0) + 8.0 * h0
     if phase == "bucketsort":
         return 16.0 * st["small_keys"] + 8.0 * (st["h1_keys"])
     if phase == "big":
