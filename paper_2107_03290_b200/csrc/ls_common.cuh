@@ -179,7 +179,9 @@ enum {
 };
 enum { STATUS_NAN = 1u, STATUS_INTERNAL = 2u };
 constexpr int BIG_LEVELS = 6;
-constexpr uint32_t WS_MAX = 256;  // SMALL sub-buckets up to this size: one warp each (k_warpsort)
+constexpr uint32_t WS_MAX = 256;  // SMALL sub-buckets of WS_MIN+1..WS_MAX keys: one warp each (k_warpsort)
+constexpr uint32_t WS_MIN = 32;   // tiny sub-buckets (<= WS_MIN keys) go to the block windows, many per window
+__host__ __device__ __forceinline__ bool warp_task_size(uint32_t np) { return np > WS_MIN && np <= WS_MAX; }
 constexpr uint32_t LARGE_MIN = 262144;  // big sub-buckets above this: grid-parallel path (ls_bigpath.cu)
 
 struct Ctl {

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     const uint32_t st = j < f ? (uint32_t)bbeg + s[j] : 0u;
     // SMALL sub-buckets of <= WS_MAX keys become warp tasks (compacted per
     // block: one global atomic per level-0 bucket)
-    const bool task = j < f && c >= 2u && c <= a.T_small && c <= WS_MAX;
+    const bool task = j < f && c <= a.T_small && warp_task_size(c);
     {
         __shared__ uint32_t wcnt[32], wbase;
         const uint32_t m = __ballot_sync(0xffffffffu, task);
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         if (c <= 1) {
             if (a.dH1) a.dH1[g] = 1;
         } else if (c <= a.T_small) {
-            if (!task) {  // middle class: block windows
+            if (!task) {  // tiny and 257..T_small: block windows
                 const uint32_t t = st / a.T_tile;
                 atomicMin(&a.tile_first[t], (uint32_t)g);
                 atomicMax(&a.tile_last[t], (uint32_t)g);

@@ -349,9 +349,9 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 uint32_t sl = (uint32_t)i;
                 // (keys of a homogeneous level-0 bucket lying inside the span
                 // have no head of their own: they stay where they are)
-                // (sub-buckets of <= WS_MAX keys are sorted by k_warpsort and
-                // stay in place here, like single keys)
-                if (np > WS_MAX && (uint32_t)i - h < np) {
+                // (sub-buckets of WS_MIN+1..WS_MAX keys are sorted by
+                // k_warpsort and stay in place here, like single keys)
+                if (np >= 2u && !warp_task_size(np) && (uint32_t)i - h < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
                     sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         for (uint32_t g = g0 + tid; g <= g1; g += BS_THREADS) {
             const bool first = g == g0 + tid;
             const uint32_t np = first ? my_np : __ldg(&a.hist1[g]);
-            if (np <= WS_MAX) continue;  // k_warpsort's
+            if (np < 2u || warp_task_size(np)) continue;  // single keys / k_warpsort's
             const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
             if (T[h] != T[h + np - 1u]) {  // sorted: homogeneous iff first == last
                 r_small++;
