@@ -41,8 +41,8 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid;
-    uint32_t task_cap, lcap, pcap;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills;
+    uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
@@ -108,6 +108,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.lhom = take((size_t)l.lcap * 32 * 4);
     l.pcap = (uint32_t)(n / 4 + 64);
     l.pieces = take((size_t)l.pcap * 8);
+    l.fcap = (uint32_t)(l.lcap * 1024 + n / 65536 + 64);
+    l.fills = take((size_t)l.fcap * 16);
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
@@ -168,6 +170,8 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.lmin = (unsigned long long *)(w + l.lmin);
     a.lmax = (unsigned long long *)(w + l.lmax);
     a.pieces = (uint2 *)(w + l.pieces);
+    a.fills = (uint4 *)(w + l.fills);
+    a.fcap = l.fcap;
     a.task_cap = l.task_cap;
     a.big = (BigItem *)(w + l.big);
     a.chunks = (BigChunk *)(w + l.chunks);

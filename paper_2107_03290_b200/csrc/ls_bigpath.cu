@@ -26,7 +26,7 @@ namespace ls {
 constexpr int LD_BITS = 10;
 constexpr int LD_DIG = 1 << LD_BITS;  // 1024 digits
 constexpr int LD_WORDS = LD_DIG / 32;
-constexpr uint32_t PIECE_MAX = 256;  // pieces up to this size: one warp (k_piece_sort)
+constexpr uint32_t PIECE_MAX = 512;  // pieces up to this size: one warp (k_piece_sort)
 
 __device__ __forceinline__ int large_shift(unsigned long long mn, unsigned long long mx) {
     const unsigned long long range = mx - mn;
@@ -103,7 +103,19 @@ __global__ void __launch_bounds__(LD_DIG) k_large_scan(Args a) {
         const bool homo = c >= 1u && a.lmin[k] == a.lmax[k];
         a.lstart[k] = st;
         a.lcur[k] = item.off + st;  // scatter cursor (k_large_scatter reserves ranges)
-        if (homo) atomicOr(&hw[d >> 5], 1u << (d & 31));
+        if (homo) {
+            atomicOr(&hw[d >> 5], 1u << (d & 31));
+            const unsigned long long o = a.lmin[k];
+            const uint32_t nf = (c + MM_CHUNK - 1) / MM_CHUNK;  // fill tasks of <= 64K keys
+            const uint32_t q = atomicAdd(&a.ctl->nfill, nf);
+            for (uint32_t x = 0; x < nf; x++) {
+                if (q + x < a.fcap)
+                    a.fills[q + x] = make_uint4(item.off + st + x * MM_CHUNK, min(MM_CHUNK, c - x * MM_CHUNK),
+                                                (uint32_t)o, (uint32_t)(o >> 32));
+                else
+                    atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+            }
+        }
         if (!homo && c >= 2u) {
             if (c <= PIECE_MAX) {
                 const uint32_t q = atomicAdd(&a.ctl->npiece, 1u);
@@ -192,32 +204,18 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_large_scatter(Args a) {
 }
 
 // ------------------------------------------------------------------ fill --
+// Homogeneous pieces: write their value (one task per <= 64K keys).
 template <int DT>
-__global__ void __launch_bounds__(512) k_large_fill(Args a) {
+__global__ void __launch_bounds__(256) k_large_fill(Args a) {
     if (a.ctl->status) return;
-    __shared__ uint32_t st[LD_DIG + 1];
-    __shared__ uint32_t hom[LD_WORDS];
-    const uint32_t nch = min(a.ctl->nchunks, a.chunk_cap);
-    for (uint32_t e = blockIdx.x; e < nch; e += gridDim.x) {
-        const BigChunk ch = a.chunks[e];
-        const BigItem item = a.big[ch.item];
-        if (item.pad0 == 0 || item.mn == item.mx || item.pad1 == 0) continue;
-        const uint32_t li = item.pad0 - 1u;
-        for (int d = threadIdx.x; d < LD_DIG; d += blockDim.x) st[d] = a.lstart[(size_t)li * LD_DIG + d];
-        if (threadIdx.x == 0) st[LD_DIG] = item.size;
-        if (threadIdx.x < LD_WORDS) hom[threadIdx.x] = a.lhom[(size_t)li * LD_WORDS + threadIdx.x];
-        __syncthreads();
-        const uint32_t beg = ch.chunk * MM_CHUNK, end = min(item.size, beg + MM_CHUNK);
-        const unsigned long long *lmin = a.lmin + (size_t)li * LD_DIG;
-        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
-            int lo = 0, hi = LD_DIG - 1;  // largest d with st[d] <= q
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (st[mid] <= q) lo = mid; else hi = mid - 1;
-            }
-            if ((hom[lo >> 5] >> (lo & 31)) & 1u) a.A[item.off + q] = from_ord<DT>(lmin[lo]);
-        }
-        __syncthreads();
+    const uint32_t nf = min(a.ctl->nfill, a.fcap);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nf; t += nw) {
+        const uint4 f = a.fills[t];
+        const uint64_t v = from_ord<DT>((unsigned long long)f.z | ((unsigned long long)f.w << 32));
+        uint64_t *dst = a.A + f.x;
+        for (uint32_t i = lane; i < f.y; i += 32) dst[i] = v;
     }
 }
 
@@ -233,34 +231,14 @@ __global__ void __launch_bounds__(256) k_piece_sort(Args a) {
         const uint32_t off = pc.x, c = pc.y;
         const uint64_t *X = a.B + off;
         uint64_t *Y = a.A + off;
-        {
-            uint64_t v[8];
-#pragma unroll
-            for (int s2 = 0; s2 < 8; s2++) {
-                const uint32_t i = 32u * s2 + lane;
-                v[s2] = i < c ? to_ord<DT>(X[i]) : ~0ull;
-            }
-            if (c <= 32u) {
-                warp_sort32(v[0], lane);
-            } else if (c <= 64u) {
-                uint64_t w[2] = {v[0], v[1]};
-                warp_sort_regs<2>(w, lane);
-                v[0] = w[0];
-                v[1] = w[1];
-            } else if (c <= 128u) {
-                uint64_t w[4] = {v[0], v[1], v[2], v[3]};
-                warp_sort_regs<4>(w, lane);
-#pragma unroll
-                for (int s2 = 0; s2 < 4; s2++) v[s2] = w[s2];
-            } else {
-                warp_sort_regs<8>(v, lane);
-            }
-#pragma unroll
-            for (int s2 = 0; s2 < 8; s2++) {
-                const uint32_t i = 32u * s2 + lane;
-                if (i < c) Y[i] = from_ord<DT>(v[s2]);
-            }
-        }
+        // stage B -> A, then sort in place (peeling few-valued pieces)
+        for (uint32_t i = lane; i < c; i += 32) Y[i] = X[i];
+        __syncwarp();
+        if (c <= 32u) warp_sort_keys<DT, 1, 16>(Y, c, lane);
+        else if (c <= 64u) warp_sort_keys<DT, 2, 16>(Y, c, lane);
+        else if (c <= 128u) warp_sort_keys<DT, 4, 16>(Y, c, lane);
+        else if (c <= 256u) warp_sort_keys<DT, 8, 16>(Y, c, lane);
+        else warp_sort_keys<DT, 16, 16>(Y, c, lane);
     }
 }
 
@@ -275,14 +253,14 @@ void launch_large(const Args &a, int dtype, cudaStream_t st) {
         k_large_scan<<<sms * 2, LD_DIG, 0, st>>>(a);
         cudaFuncSetAttribute(k_large_scatter<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_large_scatter<DT_F64><<<sms, TP_THREADS, sm, st>>>(a);
-        k_large_fill<DT_F64><<<sms * 4, 512, 0, st>>>(a);
+        k_large_fill<DT_F64><<<sms * 8, 256, 0, st>>>(a);
         k_piece_sort<DT_F64><<<sms * 8, 256, 0, st>>>(a);
     } else {
         k_large_count<DT_U64><<<sms * 4, 512, 0, st>>>(a);
         k_large_scan<<<sms * 2, LD_DIG, 0, st>>>(a);
         cudaFuncSetAttribute(k_large_scatter<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_large_scatter<DT_U64><<<sms, TP_THREADS, sm, st>>>(a);
-        k_large_fill<DT_U64><<<sms * 4, 512, 0, st>>>(a);
+        k_large_fill<DT_U64><<<sms * 8, 256, 0, st>>>(a);
         k_piece_sort<DT_U64><<<sms * 8, 256, 0, st>>>(a);
     }
 }

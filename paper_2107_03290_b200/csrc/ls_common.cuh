@@ -193,6 +193,7 @@ struct Ctl {
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
     uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
+    uint32_t nfill;                    // homogeneous pieces of large items (k_large_fill)
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
     unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
@@ -251,6 +252,8 @@ struct Args {
     uint32_t *ltot, *lstart, *lcur, *lhom;  // [lcap*1024] x3, [lcap*32]
     unsigned long long *lmin, *lmax;  // [lcap*1024]
     uint2 *pieces;                    // [pcap] small non-homogeneous pieces {off, size} (in B)
+    uint4 *fills;                     // [fcap] homogeneous pieces {off, size, ord lo, ord hi}
+    uint32_t fcap;
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]
     uint32_t chunk_cap;

@@ -30,6 +30,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = 0;
         ctl->nlarge = ctl->npiece = 0;
+        ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
         ctl->smin = ~0ull;
         ctl->smax = 0;

@@ -909,7 +909,8 @@ __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long 
 static_assert(sizeof(BsSmem) * BS_CTAS_PER_SM <= 228 * 1024, "bucket sort shared memory per SM");
 
 struct BigSmem {
-    uint64_t sk[BIG_SORT_CAP];
+    uint64_t sk[BIG_SORT_CAP + 2];          // (+2: aligned hull of a TMA-staged window)
+    uint64_t mbar;
     uint32_t start[BIG_DIGITS], end[BIG_DIGITS];
     uint32_t wlo[BIG_MAXWIN], whi[BIG_MAXWIN];
     uint32_t blk[BIG_MAXBLK];
@@ -934,6 +935,9 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
     const int nwarps = bd >> 5;
     const uint32_t cnt = min(a.ctl->big_cnt[level], a.big_cap);
     const BigItem *list = a.big + (size_t)level * a.big_cap;
+    uint32_t mphase = 0;
+    if (tid == 0) mbar_init(&S.mbar, 1);
+    __syncthreads();
     const bool prof = (a.dbg & 512u) && threadIdx.x == 0;
     long long t_prev = clock64();
 #define BG_PROF(k)                                                                  \
@@ -1072,34 +1076,49 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                 const uint32_t dlo = S.wlo[w], dhi = S.whi[w];
                 if (dlo > dhi) continue;  // uniform
                 const uint32_t slo = S.start[dlo], shi = S.end[dhi];
-                for (uint32_t i = tid; i < shi - slo; i += bd) S.sk[i] = Y[slo + i];
-                __syncthreads();
+                // stage Y[slo, shi) with the TMA bulk engine (aligned hull)
+                const uint64_t gl = item.off + slo, gh = item.off + shi;
+                if (tid == 0) {
+                    const uint64_t *Yb = item.in_b ? a.A : a.B;
+                    const uint64_t h0 = gl & ~1ull;
+                    uint64_t h1 = (gh + 1) & ~1ull;
+                    if (h1 > a.n) {
+                        h1 = gh & ~1ull;
+                        S.sk[gh - 1 - h0] = Yb[gh - 1];
+                    }
+                    const uint32_t bytes = (uint32_t)((h1 - h0) * 8);
+                    mbar_expect_tx(&S.mbar, bytes);
+                    for (uint32_t o = 0; o < bytes; o += 32768u)
+                        bulk_g2s((char *)S.sk + o, (const char *)(Yb + h0) + o,
+                                 bytes - o < 32768u ? bytes - o : 32768u, &S.mbar);
+                }
+                mbar_wait(&S.mbar, mphase);
+                mphase ^= 1u;
+                uint64_t *sk = S.sk + (gl & 1ull);
                 for (uint32_t d = dlo + tid; d <= dhi; d += bd) {  // one thread per tiny piece
                     const uint32_t pc = S.end[d] - S.start[d];
-                    if (pc >= 2 && pc <= 8) insertion_sort<DT>(S.sk + (S.start[d] - slo), (int)pc);
+                    if (pc >= 2 && pc <= 8) insertion_sort<DT>(sk + (S.start[d] - slo), (int)pc);
                 }
                 for (uint32_t d = dlo + warp; d <= dhi; d += nwarps) {  // one warp per larger piece
                     const uint32_t pc = S.end[d] - S.start[d];
                     if ((a.dbg & 512u) && lane == 0 && pc > 1)
                         atomicAdd(&a.ctl->prof[pc <= 8 ? 6 : pc <= 32 ? 7 : pc <= 64 ? 8 : pc <= 256 ? 9 : pc <= 1024 ? 10 : 11], 1ull);
                     if (pc <= 8) continue;
-                    uint64_t *g = S.sk + (S.start[d] - slo);
-                    if (pc <= 32) {  // register bitonic across the warp
-                        uint64_t v = (uint32_t)lane < pc ? to_ord<DT>(g[lane]) : ~0ull;
-                        warp_sort32(v, lane);
-                        if ((uint32_t)lane < pc) g[lane] = from_ord<DT>(v);
+                    uint64_t *g = sk + (S.start[d] - slo);
+                    if (pc <= 32) {  // registers across the warp (peel few-valued pieces)
+                        warp_sort_keys<DT, 1>(g, pc, lane);
                     } else if (pc <= 64) {
-                        warp_sort_piece<DT, 2>(g, pc, lane);
+                        warp_sort_keys<DT, 2>(g, pc, lane);
                     } else if (pc <= 128) {
-                        warp_sort_piece<DT, 4>(g, pc, lane);
+                        warp_sort_keys<DT, 4>(g, pc, lane);
                     } else if (pc <= 256) {
-                        warp_sort_piece<DT, 8>(g, pc, lane);
+                        warp_sort_keys<DT, 8>(g, pc, lane);
                     } else if (pc <= BIG_CHUNK) {
                         bitonic<DT, false>(g, (int)pc, lane, 32);
                     }
                 }
                 __syncthreads();
-                for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = S.sk[i];
+                for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
                 __syncthreads();
             }
         }

@@ -90,4 +90,58 @@ __device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int la
     }
 }
 
+// Sort pc <= 32*NS keys of g (shared or global memory, key bits; DT order) by
+// one warp. Pieces with few distinct values (duplicate-heavy inputs) are
+// emitted by peeling: up to PEEL rounds of (warp minimum of the remaining
+// keys, how many equal it, write that run); only if more distinct values
+// remain is the full register bitonic network run.
+template <int DT, int NS, int PEEL = 4>
+__device__ __forceinline__ void warp_sort_keys(uint64_t *g, uint32_t pc, int lane) {
+    uint64_t v[NS];
+    uint32_t live = 0;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const uint32_t i = 32u * s + lane;
+        v[s] = i < pc ? to_ord<DT>(g[i]) : ~0ull;
+        live |= (i < pc ? 1u : 0u) << s;
+    }
+    uint32_t out = 0;
+    for (int r = 0; r < PEEL; r++) {
+        unsigned long long m = ~0ull;
+#pragma unroll
+        for (int s = 0; s < NS; s++)
+            if ((live >> s) & 1u) m = v[s] < m ? v[s] : m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+            m = t < m ? t : m;
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+            const bool e = ((live >> s) & 1u) && v[s] == m;
+            c += e ? 1u : 0u;
+            live &= ~((e ? 1u : 0u) << s);
+        }
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
+        const uint64_t key = from_ord<DT>(m);
+        for (uint32_t i = out + lane; i < out + tot; i += 32) g[i] = key;
+        out += tot;
+        if (out >= pc) return;
+    }
+    __syncwarp();
+    // more than PEEL distinct values: sort the remaining keys (the peeled ones
+    // are the smallest and already written)
+#pragma unroll
+    for (int s = 0; s < NS; s++)
+        if (!((live >> s) & 1u)) v[s] = ~0ull;
+    warp_sort_regs<NS>(v, lane);
+    const uint32_t rem = pc - out;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const uint32_t i = 32u * s + lane;
+        if (i < rem) g[out + i] = from_ord<DT>(v[s]);
+    }
+}
+
 }  // namespace ls
