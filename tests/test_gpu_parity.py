@@ -368,3 +368,26 @@ def test_large_big_items(case):
     assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
     if case.startswith("clusters"):
         assert st["big_keys"] >= 800_000
+
+
+# ------------------------------------------- the paper's second workloads --
+
+@pytest.mark.parametrize("s", [0.5, 0.9, 0.99])
+def test_zipf_skew_sweep_bit_exact(s):
+    """Fig. 6: Zipf skews 0.5 .. 0.99 (V = 10^5 values)."""
+    plan = datagen.Plan("zipf", 2_000_000, 1, zipf_s=s, zipf_V=100_000)
+    keys = torch.empty(2_000_000, dtype=torch.uint64, device=DEV)
+    plan.device(keys)
+    torch.cuda.synchronize()
+    check_sort(keys)
+
+
+@pytest.mark.parametrize("n", [1_000_000, 4_000_000, 16_000_000])
+def test_size_sweep_bit_exact(n):
+    """Fig. 5: Normal(0,1) and TwoDups across sizes."""
+    for dist in ("normal", "twodups"):
+        keys = gen(dist, n, 0)
+        h = to_np(keys)
+        t = keys.clone()
+        ls.ls_sort(t)
+        assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
