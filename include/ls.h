@@ -56,7 +56,7 @@ typedef struct {
     uint32_t leaf_count;    /* L, 1..LS_MAX_LEAVES, default 1000            */
     uint32_t sample_stride; /* s >= 1, default 100 (strided 1% sample, R9)  */
     uint32_t fit;           /* 0 = chord fit (R7); the only fit implemented  */
-    uint32_t big_threshold; /* T_small in keys, 64..1024, default 1024       */
+    uint32_t big_threshold; /* T_small in keys, 64..4096, default 4096       */
     uint32_t reserved;
     uint64_t flags;         /* LS_FLAG_*                                      */
 } ls_config;

@@ -40,7 +40,7 @@ def _check(status: int, where: str) -> None:
 
 
 def config(fanout: int = 1000, leaf_count: int = 1000, sample_stride: int = 100,
-           big_threshold: int = 1024, flags: int = 0) -> Config:
+           big_threshold: int = 4096, flags: int = 0) -> Config:
     c = Config()
     lib.ls_config_default(C.byref(c))
     c.fanout, c.leaf_count, c.sample_stride = fanout, leaf_count, sample_stride

@@ -41,7 +41,7 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -60,7 +60,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     if (l.U0 == 0) l.U0 = 1;
     l.U1max = (uint32_t)((n + l.C1 - 1) / l.C1) + (uint32_t)l.f;
     l.T_small = cfg.big_threshold;
-    l.T_tile = cfg.big_threshold;
+    l.T_tile = 1024;  // bucket-sort windows hold tiny sub-buckets only (span <= T_tile + WS_MIN)
     l.ntiles = (uint32_t)((n + l.T_tile - 1) / l.T_tile);
     if (l.ntiles == 0) l.ntiles = 1;
     const uint64_t ff = (uint64_t)l.f * l.f;
@@ -102,6 +102,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.bid = take((size_t)(n + 16) * 2);
     l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
     l.tasks = take((size_t)l.task_cap * 16);
+    l.ctasks = take((size_t)l.task_cap * 16);
     l.large = take((size_t)l.lcap * 4);
     l.lstart = take((size_t)l.lcap * 1024 * 4);
     l.lcur = take((size_t)l.lcap * 1024 * 4);
@@ -160,6 +161,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.wlist = (uint4 *)(w + l.wlist);
     a.bid = (uint16_t *)(w + l.bid);
     a.tasks = (uint4 *)(w + l.tasks);
+    a.ctasks = (uint4 *)(w + l.ctasks);
     a.large = (uint32_t *)(w + l.large);
     a.lcap = l.lcap;
     a.pcap = l.pcap;
@@ -184,7 +186,7 @@ static ls_status check_config(const ls_config &c) {
     if (c.leaf_count < 1 || c.leaf_count > LS_MAX_LEAVES) { set_error("leaf_count out of range [1, 1024]"); return LS_E_INVALID; }
     if (c.sample_stride < 1) { set_error("sample_stride must be >= 1"); return LS_E_INVALID; }
     if (c.fit != 0) { set_error("only the chord fit (0) is implemented"); return LS_E_INVALID; }
-    if (c.big_threshold < 64 || c.big_threshold > 1024) { set_error("big_threshold out of range [64, 1024]"); return LS_E_INVALID; }
+    if (c.big_threshold < 64 || c.big_threshold > CS_MAX) { set_error("big_threshold out of range [64, 4096]"); return LS_E_INVALID; }
     return LS_OK;
 }
 
@@ -341,7 +343,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
     launch_bucketsort(a, dt, st);
-    launches += 2;
+    launches += 4;
     tm.mark(LS_PHASE_BUCKETSORT);
     launch_big_minmax(a, dt, st);
     launches++;
@@ -425,7 +427,7 @@ void ls_config_default(ls_config *c) {
     c->leaf_count = 1000;
     c->sample_stride = 100; // P:328 1% sample (R9)
     c->fit = 0;
-    c->big_threshold = 1024;
+    c->big_threshold = 4096;
     c->flags = 0;
 }
 

@@ -28,7 +28,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
-        ctl->ntask = 0;
+        ctl->ntask = ctl->nctask = 0;
         ctl->nlarge = ctl->npiece = 0;
         ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
@@ -371,26 +371,34 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     const uint32_t st = j < f ? (uint32_t)bbeg + s[j] : 0u;
     // SMALL sub-buckets of <= WS_MAX keys become warp tasks (compacted per
     // block: one global atomic per level-0 bucket)
-    const bool task = j < f && c <= a.T_small && warp_task_size(c);
+    const int sc = j < f ? size_class(c, a.T_small) : SC_TRIVIAL;
+    // warp / CTA sorts become task lists (compacted per block: one global
+    // atomic per level-0 bucket and class)
     {
-        __shared__ uint32_t wcnt[32], wbase;
-        const uint32_t m = __ballot_sync(0xffffffffu, task);
+        __shared__ uint32_t wcnt[2][32], wbase[2];
         const int lane = tid & 31, w = tid >> 5;
-        if (lane == 0) wcnt[w] = __popc(m);
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
-                const uint32_t t = wcnt[q];
-                wcnt[q] = tot;
-                tot += t;
-            }
-            wbase = tot ? atomicAdd(&a.ctl->ntask, tot) : 0u;
+        const uint32_t mw = __ballot_sync(0xffffffffu, sc == SC_WARP);
+        const uint32_t mc = __ballot_sync(0xffffffffu, sc == SC_CTA);
+        if (lane == 0) {
+            wcnt[0][w] = __popc(mw);
+            wcnt[1][w] = __popc(mc);
         }
         __syncthreads();
-        if (task) {
-            const uint32_t k = wbase + wcnt[w] + __popc(m & ((1u << lane) - 1u));
-            if (k < a.task_cap) a.tasks[k] = make_uint4(st, c, (uint32_t)g, 0u);
+        if (tid < 2) {
+            uint32_t tot = 0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
+                const uint32_t t = wcnt[tid][q];
+                wcnt[tid][q] = tot;
+                tot += t;
+            }
+            wbase[tid] = tot ? atomicAdd(tid == 0 ? &a.ctl->ntask : &a.ctl->nctask, tot) : 0u;
+        }
+        __syncthreads();
+        if (sc == SC_WARP || sc == SC_CTA) {
+            const int c2 = sc == SC_WARP ? 0 : 1;
+            const uint32_t m = c2 == 0 ? mw : mc;
+            const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m & ((1u << lane) - 1u));
+            if (k < a.task_cap) (c2 == 0 ? a.tasks : a.ctasks)[k] = make_uint4(st, c, (uint32_t)g, 0u);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }
     }
@@ -405,15 +413,13 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
             run += cnt;
         }
         a.start1[g] = st;
-        if (c <= 1) {
+        if (sc == SC_TRIVIAL) {
             if (a.dH1) a.dH1[g] = 1;
-        } else if (c <= a.T_small) {
-            if (!task) {  // tiny and 257..T_small: block windows
-                const uint32_t t = st / a.T_tile;
-                atomicMin(&a.tile_first[t], (uint32_t)g);
-                atomicMax(&a.tile_last[t], (uint32_t)g);
-            }
-        } else {
+        } else if (sc == SC_WINDOW) {  // tiny sub-buckets: block windows
+            const uint32_t t = st / a.T_tile;
+            atomicMin(&a.tile_first[t], (uint32_t)g);
+            atomicMax(&a.tile_last[t], (uint32_t)g);
+        } else if (sc == SC_BIG) {
             const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
             if (k < a.big_cap) {
                 uint32_t lrk = 0;  // large items: grid-parallel path (ls_bigpath.cu)

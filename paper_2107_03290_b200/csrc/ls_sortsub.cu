@@ -349,9 +349,9 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 uint32_t sl = (uint32_t)i;
                 // (keys of a homogeneous level-0 bucket lying inside the span
                 // have no head of their own: they stay where they are)
-                // (sub-buckets of WS_MIN+1..WS_MAX keys are sorted by
-                // k_warpsort and stay in place here, like single keys)
-                if (np >= 2u && !warp_task_size(np) && (uint32_t)i - h < np) {
+                // (only tiny sub-buckets are sorted here; the others belong
+                // to k_warpsort / k_ctasort / k_big and stay in place)
+                if (size_class(np, a.T_small) == SC_WINDOW && (uint32_t)i - h < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
                     sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
         for (uint32_t g = g0 + tid; g <= g1; g += BS_THREADS) {
             const bool first = g == g0 + tid;
             const uint32_t np = first ? my_np : __ldg(&a.hist1[g]);
-            if (np < 2u || warp_task_size(np)) continue;  // single keys / k_warpsort's
+            if (size_class(np, a.T_small) != SC_WINDOW) continue;  // other kernels' / single keys
             const uint32_t h = (first ? my_st : __ldg(&a.start1[g])) - lo;
             if (T[h] != T[h + np - 1u]) {  // sorted: homogeneous iff first == last
                 r_small++;
@@ -622,6 +622,22 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             key[k] = i < np ? a.A[st + i] : 0ull;
         }
         if (t + nw < ntask) nxt = a.tasks[t + nw];
+        // homogeneous sub-bucket (all keys equal): nothing to sort or store
+        {
+            const uint64_t k0 = __shfl_sync(0xffffffffu, key[0], 0);
+            bool diff = false;
+#pragma unroll
+            for (int k = 0; k < WS_KPL; k++) {
+                const uint32_t i = 32u * k + lane;
+                diff |= (i < np) && key[k] != k0;
+            }
+            if (!__any_sync(0xffffffffu, diff)) {
+                if (lane == 0 && a.dH1) a.dH1[g] = 1;
+                r_h1++;
+                r_h1k += np;
+                continue;
+            }
+        }
         for (uint32_t i = lane; i <= np; i += 32) W.K[i] = 0;
         __syncwarp();
         // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back)
@@ -797,6 +813,262 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         if (st_red[1]) atomicAdd(&a.ctl->stat[ST_SMALLK], st_red[1]);
         if (st_red[2]) atomicAdd(&a.ctl->stat[ST_H1S], st_red[2]);
         if (st_red[3]) atomicAdd(&a.ctl->stat[ST_H1K], st_red[3]);
+    }
+}
+
+// ------------------------------------------------------- CTA sub-bucket sort --
+// One CTA per SMALL sub-bucket of WS_MAX+1..CS_MAX keys (at n ~ 10^9 the
+// typical sub-bucket holds n/f^2 ~ 1000 keys). Same steps as k_warpsort with
+// block barriers: coalesced loads (16 per thread), pos per key (R5),
+// counting sort (K in shared memory), placement into padded T, odd-even
+// touch-up on 8 consecutive positions per thread (groups straddling two warps
+// and groups > 8 are sorted by warps), homogeneity = first == last, store.
+constexpr int CS_THREADS = 256;
+constexpr int CS_KPT = (int)CS_MAX / CS_THREADS;  // 16
+constexpr int CS_CTAS_PER_SM = 3;
+
+struct CsSmem {
+    uint64_t T[CS_MAX + CS_MAX / 8];
+    alignas(16) uint32_t K[CS_MAX + 8];
+    uint16_t slot_of[CS_MAX];
+    uint32_t big[BS_MAXBIG];
+    uint32_t wsum[33];
+    uint32_t nbig, ovf;
+    unsigned long long st[5];
+};
+
+template <int DT>
+__global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) {
+    if (a.ctl->status) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CsSmem &S = *reinterpret_cast<CsSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const PadT T{S.T, 0u};
+    const uint32_t ntask = min(a.ctl->nctask, a.task_cap);
+    const Root R = load_root(a.M);
+    if (tid < 5) S.st[tid] = 0;
+    for (uint32_t t = blockIdx.x; t < ntask; t += gridDim.x) {
+        const uint4 task = a.ctasks[t];
+        const uint32_t st = task.x, np = task.y, g = task.z;
+        uint64_t key[CS_KPT];
+#pragma unroll
+        for (int k = 0; k < CS_KPT; k++) {
+            const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
+            key[k] = i < np ? a.A[st + i] : 0ull;
+        }
+        // homogeneous sub-bucket (all keys equal): nothing to sort or store
+        {
+            const uint64_t k0 = a.A[st];
+            bool diff = false;
+#pragma unroll
+            for (int k = 0; k < CS_KPT; k++) {
+                const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
+                diff |= (i < np) && key[k] != k0;
+            }
+            if (!__syncthreads_or(diff)) {
+                if (tid == 0) {
+                    if (a.dH1) a.dH1[g] = 1;
+                    S.st[2] += 1;
+                    S.st[3] += np;
+                }
+                continue;
+            }
+        }
+        for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
+        if (tid == 0) S.nbig = S.ovf = 0;
+        __syncthreads();
+        const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
+        const double top = (double)(np - 1u);
+        uint32_t code[CS_KPT];
+#pragma unroll
+        for (int k = 0; k < CS_KPT; k++) {
+            const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
+            code[k] = BS_NONE;
+            if (i < np) {
+                const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
+                const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                const uint32_t r = atomicAdd(&S.K[pos], 1u);
+                code[k] = pos | (r << 12);
+            }
+        }
+        __syncthreads();
+        // exclusive running totals over np + 1 <= 4097 entries, 17 per thread
+        {
+            constexpr int PER = (CS_MAX + CS_THREADS) / CS_THREADS;  // 17
+            uint32_t v[PER];
+            uint32_t sum = 0, mg = 0;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const uint32_t idx = PER * tid + q;
+                const uint32_t c = idx < np ? S.K[idx] : 0u;
+                mg = c > mg ? c : mg;
+                if (c > BS_RANKMAX) {
+                    const uint32_t j = atomicAdd(&S.nbig, 1u);
+                    if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
+                }
+                v[q] = sum;
+                sum += c;
+            }
+            mg = __reduce_max_sync(0xffffffffu, mg);
+            if (lane == 0 && mg > 1u) atomicMax(&S.st[4], (unsigned long long)mg);
+            const uint32_t incl = warp_incl_scan(sum);
+            if (lane == 31) S.wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < CS_THREADS / 32 ? S.wsum[lane] : 0u;
+                S.wsum[lane] = warp_incl_scan(w) - w;
+            }
+            __syncthreads();
+            const uint32_t off = S.wsum[warp] + incl - sum;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const uint32_t idx = PER * tid + q;
+                if (idx <= np) S.K[idx] = v[q] + off;
+            }
+        }
+        __syncthreads();
+        // placement
+#pragma unroll
+        for (int k = 0; k < CS_KPT; k++) {
+            if (code[k] != BS_NONE) {
+                const uint32_t pos = code[k] & 0xfffu;
+                const uint32_t q = S.K[pos] + (code[k] >> 12);
+                T[q] = to_ord<DT>(key[k]);
+                S.slot_of[q] = (uint16_t)pos;
+            }
+        }
+        __syncthreads();
+        // touch-up: odd-even between equal-slot neighbours, 16 consecutive
+        // positions per thread as two rows of 8 (within a warp's 512 positions)
+        for (int half = 0; half < 2; half++) {
+            const uint32_t row_i = (uint32_t)(half * CS_THREADS + tid);  // row of 8 positions
+            const uint32_t q0 = 8u * row_i;
+            uint64_t v[8];
+            uint32_t sv[8];
+            {
+                const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i];
+                const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i + 1];
+                const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
+                const uint64_t *row = S.T + 9u * row_i;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const bool in = q0 + q < np;
+                    v[q] = in ? row[q] : ~0ull;
+                    sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
+                }
+            }
+            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
+                const bool sw_ = sx == sy && x > y;
+                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
+                x = lo_;
+                y = hi_;
+                return sw_;
+            };
+            for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
+                bool any = false;
+                any |= cx(v[0], v[1], sv[0], sv[1]);
+                any |= cx(v[2], v[3], sv[2], sv[3]);
+                any |= cx(v[4], v[5], sv[4], sv[5]);
+                any |= cx(v[6], v[7], sv[6], sv[7]);
+                any |= cx(v[1], v[2], sv[1], sv[2]);
+                any |= cx(v[3], v[4], sv[3], sv[4]);
+                any |= cx(v[5], v[6], sv[5], sv[6]);
+                const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
+                const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
+                const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
+                const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
+                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                if (!__any_sync(0xffffffffu, any)) break;
+            }
+            if (q0 < np) {
+                uint64_t *row = S.T + 9u * row_i;
+#pragma unroll
+                for (int q = 0; q < 8; q++) row[q] = v[q];
+            }
+            // a small group straddling two warps' 256-position ranges
+            if (lane == 0 && row_i > 0 && q0 < np && sv[0] < 0x10000u && S.slot_of[q0 - 1] == sv[0]) {
+                const uint32_t sl = sv[0], c = S.K[sl + 1] - S.K[sl];
+                if (c <= BS_RANKMAX) {
+                    const uint32_t j = atomicAdd(&S.nbig, 1u);
+                    if (j < BS_MAXBIG) S.big[j] = sl; else S.ovf = 1;
+                }
+            }
+        }
+        __syncthreads();
+        // listed groups: one warp each
+        {
+            const uint32_t nb = min(S.nbig, (uint32_t)BS_MAXBIG);
+            const uint32_t extra = S.ovf ? np : 0u;
+            for (uint32_t k = warp; k < nb + extra; k += CS_THREADS / 32) {
+                uint32_t sl;
+                if (k < nb) {
+                    sl = S.big[k];
+                } else {  // overflow: sort every multi-key group again (rare; idempotent)
+                    sl = k - nb;
+                    if (S.K[sl + 1] - S.K[sl] < 2u) continue;
+                }
+                const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
+                if (c <= BS_RANKMAX) {
+                    if (lane == 0) {
+                        for (uint32_t x = 1; x < c; x++) {
+                            const uint64_t tt = T[base + x];
+                            uint32_t y = x;
+                            while (y > 0 && T[base + y - 1] > tt) {
+                                T[base + y] = T[base + y - 1];
+                                y--;
+                            }
+                            T[base + y] = tt;
+                        }
+                    }
+                    continue;
+                }
+                bool same = true;
+                for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
+                if (__all_sync(0xffffffffu, same)) continue;
+                if (c <= 32u) {
+                    uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
+                    warp_sort32(v1, lane);
+                    if ((uint32_t)lane < c) T[base + lane] = v1;
+                } else if (c <= 64u) {
+                    warp_sort_T<2>(T + base, c, lane);
+                } else if (c <= 128u) {
+                    warp_sort_T<4>(T + base, c, lane);
+                } else if (c <= 256u) {
+                    warp_sort_T<8>(T + base, c, lane);
+                } else {
+                    bitonic_view(T + base, (int)c, lane, 32);
+                }
+            }
+        }
+        __syncthreads();
+        // homogeneous iff first == last of the sorted sub-bucket
+        const bool homog = T[0] == T[np - 1u];
+        if (!homog) {
+#pragma unroll
+            for (int k = 0; k < CS_KPT; k++) {
+                const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
+                if (i < np) a.A[st + i] = from_ord<DT>(T[i]);
+            }
+        }
+        if (tid == 0) {
+            if (!homog) {
+                S.st[0] += 1;
+                S.st[1] += np;
+            } else {
+                if (a.dH1) a.dH1[g] = 1;
+                S.st[2] += 1;
+                S.st[3] += np;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (S.st[0]) atomicAdd(&a.ctl->stat[ST_SMALLS], S.st[0]);
+        if (S.st[1]) atomicAdd(&a.ctl->stat[ST_SMALLK], S.st[1]);
+        if (S.st[2]) atomicAdd(&a.ctl->stat[ST_H1S], S.st[2]);
+        if (S.st[3]) atomicAdd(&a.ctl->stat[ST_H1K], S.st[3]);
+        if (S.st[4]) atomicMax(&a.ctl->stat[ST_MAXGRP], S.st[4]);
     }
 }
 
@@ -1146,6 +1418,15 @@ void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
         const int g = sms * WS_CTAS_PER_SM;
         if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
         else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
+        const size_t csm = sizeof(CsSmem);
+        const int gc = sms * CS_CTAS_PER_SM;
+        if (dtype == DT_F64) {
+            cudaFuncSetAttribute(k_ctasort<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+            k_ctasort<DT_F64><<<gc, CS_THREADS, csm, st>>>(a);
+        } else {
+            cudaFuncSetAttribute(k_ctasort<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+            k_ctasort<DT_U64><<<gc, CS_THREADS, csm, st>>>(a);
+        }
     }
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);

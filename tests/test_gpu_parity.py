@@ -228,7 +228,7 @@ def test_other_fanouts(f, L, stride, n):
                ocfg=O.config(fanout=f, leaf_count=L, sample_stride=stride), f=f)
 
 
-@pytest.mark.parametrize("thr", [64, 512, 1024])
+@pytest.mark.parametrize("thr", [64, 512, 1024, 4096])
 def test_big_threshold(thr):
     """Small thresholds push sub-buckets through the exact big path."""
     for dist in ("telemetry", "normal"):
