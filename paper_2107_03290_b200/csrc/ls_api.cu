@@ -41,7 +41,7 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -103,6 +103,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
     l.tasks = take((size_t)l.task_cap * 16);
     l.ctasks = take((size_t)l.task_cap * 16);
+    l.ctasks2 = take((size_t)l.task_cap * 16);
     l.large = take((size_t)l.lcap * 4);
     l.lstart = take((size_t)l.lcap * 1024 * 4);
     l.lcur = take((size_t)l.lcap * 1024 * 4);
@@ -162,6 +163,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.bid = (uint16_t *)(w + l.bid);
     a.tasks = (uint4 *)(w + l.tasks);
     a.ctasks = (uint4 *)(w + l.ctasks);
+    a.ctasks2 = (uint4 *)(w + l.ctasks2);
     a.large = (uint32_t *)(w + l.large);
     a.lcap = l.lcap;
     a.pcap = l.pcap;
@@ -343,7 +345,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
     launch_bucketsort(a, dt, st);
-    launches += 4;
+    launches += 5;
     tm.mark(LS_PHASE_BUCKETSORT);
     launch_big_minmax(a, dt, st);
     launches++;

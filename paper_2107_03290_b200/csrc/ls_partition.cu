@@ -28,7 +28,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
-        ctl->ntask = ctl->nctask = 0;
+        ctl->ntask = ctl->nctask = ctl->nctask2 = 0;
         ctl->nlarge = ctl->npiece = 0;
         ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
@@ -375,30 +375,31 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     // warp / CTA sorts become task lists (compacted per block: one global
     // atomic per level-0 bucket and class)
     {
-        __shared__ uint32_t wcnt[2][32], wbase[2];
+        __shared__ uint32_t wcnt[3][32], wbase[3];
         const int lane = tid & 31, w = tid >> 5;
-        const uint32_t mw = __ballot_sync(0xffffffffu, sc == SC_WARP);
-        const uint32_t mc = __ballot_sync(0xffffffffu, sc == SC_CTA);
-        if (lane == 0) {
-            wcnt[0][w] = __popc(mw);
-            wcnt[1][w] = __popc(mc);
-        }
+        uint32_t m[3];
+        m[0] = __ballot_sync(0xffffffffu, sc == SC_WARP);
+        m[1] = __ballot_sync(0xffffffffu, sc == SC_CTA);
+        m[2] = __ballot_sync(0xffffffffu, sc == SC_CTAM);
+        if (lane == 0)
+            for (int q = 0; q < 3; q++) wcnt[q][w] = __popc(m[q]);
         __syncthreads();
-        if (tid < 2) {
+        if (tid < 3) {
             uint32_t tot = 0;
             for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
                 const uint32_t t = wcnt[tid][q];
                 wcnt[tid][q] = tot;
                 tot += t;
             }
-            wbase[tid] = tot ? atomicAdd(tid == 0 ? &a.ctl->ntask : &a.ctl->nctask, tot) : 0u;
+            uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask : &a.ctl->nctask2;
+            wbase[tid] = tot ? atomicAdd(ctr, tot) : 0u;
         }
         __syncthreads();
-        if (sc == SC_WARP || sc == SC_CTA) {
-            const int c2 = sc == SC_WARP ? 0 : 1;
-            const uint32_t m = c2 == 0 ? mw : mc;
-            const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m & ((1u << lane) - 1u));
-            if (k < a.task_cap) (c2 == 0 ? a.tasks : a.ctasks)[k] = make_uint4(st, c, (uint32_t)g, 0u);
+        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : -1;
+        if (c2 >= 0) {
+            const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m[c2] & ((1u << lane) - 1u));
+            uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : a.ctasks2;
+            if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, 0u);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }
     }

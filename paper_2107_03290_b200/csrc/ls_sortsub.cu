@@ -356,7 +356,13 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
                     sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
                 }
-                const uint32_t r = atomicAdd(&S.K[sl], 1u);
+                // warp-aggregated: keys of equal slot (duplicates!) take one atomic
+                const uint32_t peers = __match_any_sync(__activemask(), sl);
+                const int leader = __ffs(peers) - 1;
+                uint32_t r0 = 0;
+                if (lane == leader) r0 = atomicAdd(&S.K[sl], (uint32_t)__popc(peers));
+                r0 = __shfl_sync(peers, r0, leader);
+                const uint32_t r = r0 + __popc(peers & ((1u << lane) - 1u));
                 code[k] = sl | (r << BS_LOG_W);
             }
         }
@@ -823,32 +829,36 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 // counting sort (K in shared memory), placement into padded T, odd-even
 // touch-up on 8 consecutive positions per thread (groups straddling two warps
 // and groups > 8 are sorted by warps), homogeneity = first == last, store.
-constexpr int CS_THREADS = 256;
-constexpr int CS_KPT = (int)CS_MAX / CS_THREADS;  // 16
-constexpr int CS_CTAS_PER_SM = 3;
+constexpr int CS_KPT = 16;  // keys per thread; capacity = 16 x threads
 
+template <int CAP>
 struct CsSmem {
-    uint64_t T[CS_MAX + CS_MAX / 8];
-    alignas(16) uint32_t K[CS_MAX + 8];
-    uint16_t slot_of[CS_MAX];
+    uint64_t T[CAP + CAP / 8];
+    uint32_t mixed[CAP / 32];               // per pos: its group holds >= 2 distinct keys
+    alignas(16) uint32_t K[CAP + 8];
+    uint16_t slot_of[CAP];
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
     uint32_t nbig, ovf;
     unsigned long long st[5];
 };
 
-template <int DT>
-__global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) {
+// CS_THREADS = 256 for 2049..4096 keys (3 CTAs/SM), 128 for 257..2048 (6 CTAs/SM:
+// more tasks in flight where a task is short and latency-bound).
+template <int DT, int CS_THREADS, int CS_CTAS_PER_SM>
+__global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, const uint4 *list,
+                                                                     const uint32_t *count) {
     if (a.ctl->status) return;
+    constexpr int CAP = CS_THREADS * CS_KPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CsSmem &S = *reinterpret_cast<CsSmem *>(smem_raw);
+    CsSmem<CAP> &S = *reinterpret_cast<CsSmem<CAP> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PadT T{S.T, 0u};
-    const uint32_t ntask = min(a.ctl->nctask, a.task_cap);
+    const uint32_t ntask = min(*count, a.task_cap);
     const Root R = load_root(a.M);
     if (tid < 5) S.st[tid] = 0;
     for (uint32_t t = blockIdx.x; t < ntask; t += gridDim.x) {
-        const uint4 task = a.ctasks[t];
+        const uint4 task = list[t];
         const uint32_t st = task.x, np = task.y, g = task.z;
         uint64_t key[CS_KPT];
 #pragma unroll
@@ -875,6 +885,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
             }
         }
         for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
+        for (uint32_t i = tid; i < (np + 31) / 32; i += CS_THREADS) S.mixed[i] = 0;
         if (tid == 0) S.nbig = S.ovf = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
@@ -892,21 +903,19 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
             }
         }
         __syncthreads();
-        // exclusive running totals over np + 1 <= 4097 entries, 17 per thread
+        // exclusive running totals over np + 1 <= 4097 entries: each thread a
+        // contiguous segment of ceil((np + 1) / 256) entries (cost ~ np)
         {
-            constexpr int PER = (CS_MAX + CS_THREADS) / CS_THREADS;  // 17
-            uint32_t v[PER];
+            const uint32_t per = (np + CS_THREADS) / CS_THREADS;
+            const uint32_t b0 = per * tid, b1 = min(b0 + per, np + 1u);
             uint32_t sum = 0, mg = 0;
-#pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const uint32_t idx = PER * tid + q;
+            for (uint32_t idx = b0; idx < b1; idx++) {
                 const uint32_t c = idx < np ? S.K[idx] : 0u;
                 mg = c > mg ? c : mg;
                 if (c > BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
                 }
-                v[q] = sum;
                 sum += c;
             }
             mg = __reduce_max_sync(0xffffffffu, mg);
@@ -919,11 +928,11 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
                 S.wsum[lane] = warp_incl_scan(w) - w;
             }
             __syncthreads();
-            const uint32_t off = S.wsum[warp] + incl - sum;
-#pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const uint32_t idx = PER * tid + q;
-                if (idx <= np) S.K[idx] = v[q] + off;
+            uint32_t run = S.wsum[warp] + incl - sum;
+            for (uint32_t idx = b0; idx < b1; idx++) {
+                const uint32_t c = idx < np ? S.K[idx] : 0u;
+                S.K[idx] = run;
+                run += c;
             }
         }
         __syncthreads();
@@ -939,8 +948,8 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
         }
         __syncthreads();
         // touch-up: odd-even between equal-slot neighbours, 16 consecutive
-        // positions per thread as two rows of 8 (within a warp's 512 positions)
-        for (int half = 0; half < 2; half++) {
+        // positions per thread as two rows of 8 (the second only if np > 2048)
+        for (int half = 0; half < (np > 8u * CS_THREADS ? 2 : 1); half++) {
             const uint32_t row_i = (uint32_t)(half * CS_THREADS + tid);  // row of 8 positions
             const uint32_t q0 = 8u * row_i;
             uint64_t v[8];
@@ -955,6 +964,29 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
                     const bool in = q0 + q < np;
                     v[q] = in ? row[q] : ~0ull;
                     sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
+                }
+            }
+            // mixed-group flags (adjacent equal-slot pairs with different keys;
+            // the pair across two rows is checked from the row on the left,
+            // using shared memory at warp boundaries)
+            {
+                uint64_t nv0 = __shfl_down_sync(0xffffffffu, v[0], 1);
+                uint32_t ns0 = __shfl_down_sync(0xffffffffu, sv[0], 1);
+                if (lane == 31) {
+                    const uint32_t qn = q0 + 8u;
+                    if (qn < np) {
+                        nv0 = S.T[9u * (row_i + 1u)];
+                        ns0 = S.slot_of[qn];
+                    } else {
+                        ns0 = 0xfffffu;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const uint64_t y = q < 7 ? v[q + 1] : nv0;
+                    const uint32_t sy = q < 7 ? sv[q + 1] : ns0;
+                    if (sv[q] < 0x10000u && sv[q] == sy && v[q] != y)
+                        atomicOr(&S.mixed[sv[q] >> 5], 1u << (sv[q] & 31u));
                 }
             }
             auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
@@ -1008,6 +1040,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
                     sl = k - nb;
                     if (S.K[sl + 1] - S.K[sl] < 2u) continue;
                 }
+                if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
                 if (c <= BS_RANKMAX) {
                     if (lane == 0) {
@@ -1023,9 +1056,6 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a) 
                     }
                     continue;
                 }
-                bool same = true;
-                for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
-                if (__all_sync(0xffffffffu, same)) continue;
                 if (c <= 32u) {
                     uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
                     warp_sort32(v1, lane);
@@ -1410,6 +1440,20 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
 }
 
 // -------------------------------------------------------------- launchers --
+template <int NT, int PER_SM>
+static void launch_ctasort(const Args &a, int dtype, cudaStream_t st, const uint4 *list,
+                           const uint32_t *count, int sms) {
+    const size_t sm = sizeof(CsSmem<NT * CS_KPT>);
+    const int g = sms * PER_SM;
+    if (dtype == DT_F64) {
+        cudaFuncSetAttribute(k_ctasort<DT_F64, NT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_ctasort<DT_F64, NT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
+    } else {
+        cudaFuncSetAttribute(k_ctasort<DT_U64, NT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_ctasort<DT_U64, NT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
+    }
+}
+
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
     {
         int dev = 0, sms = 148;
@@ -1418,15 +1462,8 @@ void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
         const int g = sms * WS_CTAS_PER_SM;
         if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
         else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
-        const size_t csm = sizeof(CsSmem);
-        const int gc = sms * CS_CTAS_PER_SM;
-        if (dtype == DT_F64) {
-            cudaFuncSetAttribute(k_ctasort<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-            k_ctasort<DT_F64><<<gc, CS_THREADS, csm, st>>>(a);
-        } else {
-            cudaFuncSetAttribute(k_ctasort<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-            k_ctasort<DT_U64><<<gc, CS_THREADS, csm, st>>>(a);
-        }
+        launch_ctasort<256, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
+        launch_ctasort<128, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
     }
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
