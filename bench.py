@@ -304,6 +304,39 @@ def run_ours(args):
                        "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                        "ms_per_step": statistics.mean(e2e_ms), "api": "ls_sort_host"}
 
+    # e2e (multi-GPU): host shard -> device (pinned, H2D inside the timed region),
+    # ls_sort_multi, this rank's sorted slice -> host; max over ranks
+    if multi and not args.no_e2e:
+        try:
+            host_in = torch.empty(n, dtype=tdt, pin_memory=True)
+            host_in.copy_(pristine.cpu())
+            host_out = torch.empty(out.numel(), dtype=tdt, pin_memory=True)
+            e2e_ms = []
+            for i in range(max(1, min(args.steps, 3)) + 1):
+                if world > 1:
+                    dist.barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                keys.copy_(host_in, non_blocking=True)
+                n_out2, _ = ls.ls_sort_multi(comm, keys, out, cfg=cfg, ws=ws, stream=stream)
+                host_out[:n_out2].copy_(out[:n_out2], non_blocking=True)
+                e1.record(stream)
+                e1.synchronize()
+                if i > 0:
+                    e2e_ms.append(e0.elapsed_time(e1))
+            t = sum(e2e_ms)
+            if world > 1:
+                tt = torch.tensor([t], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            ms = t / len(e2e_ms)
+            line["e2e"] = {"value": n * world / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                           "d2h_bytes_per_step": 8 * n_out, "ms_per_step": ms,
+                           "api": "ls_sort_multi (torch pinned copies around it)"}
+        except RuntimeError as e:  # pinned host memory unavailable
+            line["e2e"] = {"value": None, "unit": UNIT, "unavailable": str(e)[:200]}
+
     # CPU baseline: the oracle as it stands, rank 0 at N=1, bounded sample
     if not multi and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(plan, args.cpu_sample)

@@ -1394,20 +1394,29 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                         bulk_g2s((char *)S.sk + o, (const char *)(Yb + h0) + o,
                                  bytes - o < 32768u ? bytes - o : 32768u, &S.mbar);
                 }
+                BG_PROF(5);
                 mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
+                BG_PROF(6);
                 uint64_t *sk = S.sk + (gl & 1ull);
                 for (uint32_t d = dlo + tid; d <= dhi; d += bd) {  // one thread per tiny piece
                     const uint32_t pc = S.end[d] - S.start[d];
                     if (pc >= 2 && pc <= 8) insertion_sort<DT>(sk + (S.start[d] - slo), (int)pc);
                 }
+                BG_PROF(7);
                 for (uint32_t d = dlo + warp; d <= dhi; d += nwarps) {  // one warp per larger piece
                     const uint32_t pc = S.end[d] - S.start[d];
                     if ((a.dbg & 512u) && lane == 0 && pc > 1)
                         atomicAdd(&a.ctl->prof[pc <= 8 ? 6 : pc <= 32 ? 7 : pc <= 64 ? 8 : pc <= 256 ? 9 : pc <= 1024 ? 10 : 11], 1ull);
                     if (pc <= 8) continue;
                     uint64_t *g = sk + (S.start[d] - slo);
-                    if (pc <= 32) {  // registers across the warp (peel few-valued pieces)
+                    if (shift <= 32 && pc <= 256) {  // piece within 2^32 ords: 32-bit peeling
+                        const unsigned long long pbase = mn + ((unsigned long long)d << shift);
+                        if (pc <= 32) warp_sort_keys_rel<DT, 1>(g, pc, pbase, lane);
+                        else if (pc <= 64) warp_sort_keys_rel<DT, 2>(g, pc, pbase, lane);
+                        else if (pc <= 128) warp_sort_keys_rel<DT, 4>(g, pc, pbase, lane);
+                        else warp_sort_keys_rel<DT, 8>(g, pc, pbase, lane);
+                    } else if (pc <= 32) {  // registers across the warp (peel few-valued pieces)
                         warp_sort_keys<DT, 1>(g, pc, lane);
                     } else if (pc <= 64) {
                         warp_sort_keys<DT, 2>(g, pc, lane);
@@ -1420,8 +1429,10 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                     }
                 }
                 __syncthreads();
+                BG_PROF(8);
                 for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
                 __syncthreads();
+                BG_PROF(9);
             }
         }
         BG_PROF(3);

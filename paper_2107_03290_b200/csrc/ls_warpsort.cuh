@@ -144,4 +144,52 @@ __device__ __forceinline__ void warp_sort_keys(uint64_t *g, uint32_t pc, int lan
     }
 }
 
+// Same for a piece whose ords all lie in [base, base + 2^32): peeling works on
+// 32-bit offsets with single-instruction warp reductions (REDUX), so a piece
+// with up to PEEL distinct values costs PEEL short rounds.
+template <int DT, int NS, int PEEL = 16>
+__device__ __forceinline__ void warp_sort_keys_rel(uint64_t *g, uint32_t pc, unsigned long long base,
+                                                   int lane) {
+    uint32_t v[NS];
+    uint32_t live = 0;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const uint32_t i = 32u * s + lane;
+        v[s] = i < pc ? (uint32_t)(to_ord<DT>(g[i]) - base) : 0xffffffffu;
+        live |= (i < pc ? 1u : 0u) << s;
+    }
+    uint32_t out = 0;
+    for (int r = 0; r < PEEL; r++) {
+        uint32_t m = 0xffffffffu;
+#pragma unroll
+        for (int s = 0; s < NS; s++)
+            if ((live >> s) & 1u) m = v[s] < m ? v[s] : m;
+        m = __reduce_min_sync(0xffffffffu, m);
+        uint32_t c = 0;
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+            const bool e = ((live >> s) & 1u) && v[s] == m;
+            c += e ? 1u : 0u;
+            live &= ~((e ? 1u : 0u) << s);
+        }
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
+        const uint64_t key = from_ord<DT>(base + m);
+        for (uint32_t i = out + lane; i < out + tot; i += 32) g[i] = key;
+        out += tot;
+        if (out >= pc) return;
+    }
+    __syncwarp();
+    // more than PEEL distinct values: bitonic on the remaining offsets
+    uint64_t w[NS];
+#pragma unroll
+    for (int s = 0; s < NS; s++) w[s] = ((live >> s) & 1u) ? (uint64_t)v[s] : ~0ull;
+    warp_sort_regs<NS>(w, lane);
+    const uint32_t rem = pc - out;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const uint32_t i = 32u * s + lane;
+        if (i < rem) g[out + i] = from_ord<DT>(base + w[s]);
+    }
+}
+
 }  // namespace ls
