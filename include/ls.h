@@ -112,8 +112,9 @@ const char *ls_status_string(ls_status s);
 const char *ls_last_error(void);
 
 /* Device workspace needed by ls_sort / ls_sort_with_model / ls_train_rmi /
- * ls_bucket_ids for n keys (CUB-style size query). About 8n + O(n/64K * f)
- * bytes: the scratch copy B of Alg. 2's partition rounds plus per-unit tables. */
+ * ls_bucket_ids for n keys (CUB-style size query). About 12n bytes + ~60 MB:
+ * the scratch copy B of Alg. 2's partition rounds (8n), the round-1 bucket
+ * ids (2n), the in-bucket task lists and big-item lists, per-unit tables. */
 ls_status ls_workspace_bytes(uint64_t n, ls_dtype dtype, const ls_config *cfg, size_t *bytes);
 
 /* Fit F_A on a sample (north_star (1); R7-R9): d_sample holds m

@@ -108,7 +108,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.lstart = take((size_t)l.lcap * 1024 * 4);
     l.lcur = take((size_t)l.lcap * 1024 * 4);
     l.lhom = take((size_t)l.lcap * 32 * 4);
-    l.pcap = (uint32_t)(n / 4 + 64);
+    l.pcap = (uint32_t)(n / 256 + 1024);  // pieces come from giant items only (<= 1024 each)
     l.pieces = take((size_t)l.pcap * 8);
     l.fcap = (uint32_t)(l.lcap * 1024 + n / 65536 + 64);
     l.fills = take((size_t)l.fcap * 16);
