@@ -407,11 +407,16 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         // offs1: per-unit counts (k_count1) -> this unit's offset inside sub-bucket j
         const uint32_t u0 = a.unit1_start[b], u1 = a.unit1_start[b + 1];
         uint32_t run = 0;
-        for (uint32_t u = u0; u < u1; u++) {
-            uint32_t *o = &a.offs1[(uint64_t)u * f + j];
-            const uint32_t cnt = *o;
-            *o = run;
-            run += cnt;
+        for (uint32_t u = u0; u < u1; u += 8) {  // 8 independent loads in flight
+            uint32_t cnt[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                cnt[q] = u + q < u1 ? a.offs1[(uint64_t)(u + q) * f + j] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                if (u + q < u1) a.offs1[(uint64_t)(u + q) * f + j] = run;
+                run += cnt[q];
+            }
         }
         a.start1[g] = st;
         if (sc == SC_TRIVIAL) {
