@@ -21,6 +21,7 @@
 #include "ls_api_internal.h"
 #include "ls_launch.h"
 #include "ls_tile.cuh"
+#include "ls_tilepart.cuh"
 
 struct ls_comm {
     ncclComm_t comm;
@@ -135,22 +136,27 @@ __global__ void __launch_bounds__(512) k_dest_count(MultiArgs a) {
     }
 }
 
+// Scatter by destination rank into the send buffer: the TMA tile engine
+// (ls_tilepart.cuh) with R <= 64 buckets, so runs are long and coalesced.
+struct DestSmem {
+    TpSmem tp;
+    uint32_t base[LS_MAX_FANOUT];
+    Tagged spl[MAX_WORLD];
+};
+
 template <int DT>
-__global__ void __launch_bounds__(512) k_dest_scatter(MultiArgs a) {
-    constexpr int KPT = 8;
+__global__ void __launch_bounds__(TP_THREADS, 1) k_dest_scatter(MultiArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ Tagged spl[MAX_WORLD];
-    __shared__ uint32_t base[MAX_WORLD], cnt[MAX_WORLD], tst[MAX_WORLD], tmp[36];
-    uint64_t *skeys = (uint64_t *)smem_raw;
-    uint16_t *sbin = (uint16_t *)(skeys + KPT * blockDim.x);
+    DestSmem &S = *reinterpret_cast<DestSmem *>(smem_raw);
     const int tid = threadIdx.x, R = a.world;
     const uint64_t u = blockIdx.x;
-    if (tid < R - 1) spl[tid] = a.spl[tid];
-    if (tid < R) base[tid] = (uint32_t)a.sdispl[tid] + a.offs[u * R + tid];
-    __syncthreads();
+    if (tid < R - 1) S.spl[tid] = a.spl[tid];
+    if (tid < R) S.base[tid] = (uint32_t)a.sdispl[tid] + a.offs[u * R + tid];
+    tp_init(S.tp);
     const uint64_t beg = u * MULTI_UNIT, end = umin64(a.n, beg + MULTI_UNIT);
-    const DestBucket<DT> bf{spl, R, a.rank};
-    tile_scatter<KPT>(a.in, a.send, beg, end, base, cnt, tst, skeys, sbin, tmp, R, bf);
+    const DestBucket<DT> bf{S.spl, R, a.rank};
+    uint32_t phase = 0;
+    tile_partition(S.tp, a.in, a.send, beg, end, a.n, S.base, R, bf, phase);
 }
 
 static bool tagged_lt(const ls_tagged &x, const ls_tagged &y) {
@@ -369,13 +375,13 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     // 5. scatter by destination into the send buffer
     CUDA_CHECK(cudaMemcpyAsync(w + l.sdispl, sd.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
     if (n_in) {
-        const size_t sm = 8 * 512 * 8 + 8 * 512 * 2;
+        const size_t sm = sizeof(DestSmem);
         if (dt == DT_F64) {
             cudaFuncSetAttribute(k_dest_scatter<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_dest_scatter<DT_F64><<<l.U, 512, sm, st>>>(a);
+            k_dest_scatter<DT_F64><<<l.U, TP_THREADS, sm, st>>>(a);
         } else {
             cudaFuncSetAttribute(k_dest_scatter<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_dest_scatter<DT_U64><<<l.U, 512, sm, st>>>(a);
+            k_dest_scatter<DT_U64><<<l.U, TP_THREADS, sm, st>>>(a);
         }
     }
     CUDA_CHECK(cudaGetLastError());
