@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         }
         __syncwarp();
         // exclusive running totals over np + 1 <= 257 entries, 9 per lane
+        uint32_t mgs = 0;  // largest collision group of <= BS_RANKMAX keys
         {
             constexpr int PER = 9;
             uint32_t v[PER];
@@ -672,6 +673,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 const uint32_t idx = PER * lane + q;
                 const uint32_t c = idx < np ? W.K[idx] : 0u;
                 mg = c > mg ? c : mg;
+                mgs = (c <= BS_RANKMAX && c > mgs) ? c : mgs;
                 bigm |= (c > BS_RANKMAX ? 1u : 0u) << q;
                 v[q] = sum;
                 sum += c;
@@ -684,6 +686,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 if (idx <= np) W.K[idx] = v[q] + off;
             }
             mg = __reduce_max_sync(0xffffffffu, mg);
+            mgs = __reduce_max_sync(0xffffffffu, mgs);
             r_maxg = mg > r_maxg ? mg : r_maxg;
             // list the groups > 8 (pos values) for the warp sorts below
             const uint32_t nbl = __popc(bigm);
@@ -711,8 +714,10 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         }
         __syncwarp();
         // touch-up: odd-even transposition between equal-slot neighbours on
-        // 8 consecutive positions per lane (<= 8 rounds, early exit)
-        {
+        // 8 consecutive positions per lane; groups of <= mgs keys are sorted by
+        // mgs rounds (2 per iteration), none at all without collisions
+        const int iters = (int)((mgs + 1u) >> 1);
+        if (iters > 0) {
             const uint32_t q0 = 8u * lane;
             uint64_t v[8];
             uint32_t sv[8];
@@ -735,22 +740,20 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 y = hi_;
                 return sw_;
             };
-            for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
-                bool any = false;
-                any |= cx(v[0], v[1], sv[0], sv[1]);
-                any |= cx(v[2], v[3], sv[2], sv[3]);
-                any |= cx(v[4], v[5], sv[4], sv[5]);
-                any |= cx(v[6], v[7], sv[6], sv[7]);
-                any |= cx(v[1], v[2], sv[1], sv[2]);
-                any |= cx(v[3], v[4], sv[3], sv[4]);
-                any |= cx(v[5], v[6], sv[5], sv[6]);
+            for (int it2 = 0; it2 < iters; it2++) {
+                cx(v[0], v[1], sv[0], sv[1]);
+                cx(v[2], v[3], sv[2], sv[3]);
+                cx(v[4], v[5], sv[4], sv[5]);
+                cx(v[6], v[7], sv[6], sv[7]);
+                cx(v[1], v[2], sv[1], sv[2]);
+                cx(v[3], v[4], sv[3], sv[4]);
+                cx(v[5], v[6], sv[5], sv[6]);
                 const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
                 const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
                 const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
-                if (!__any_sync(0xffffffffu, any)) break;
+                if (lane < 31 && sv[7] == ns && v[7] > nv) v[7] = nv;
+                if (lane > 0 && ps == sv[0] && pv > v[0]) v[0] = pv;
             }
             if (q0 < np) {
                 uint64_t *row = W.T + 9u * lane;
