@@ -715,7 +715,8 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         __syncwarp();
         // touch-up: odd-even transposition between equal-slot neighbours on
         // 8 consecutive positions per lane; groups of <= mgs keys are sorted by
-        // mgs rounds (2 per iteration), none at all without collisions
+        // mgs rounds (2 per iteration), none at all without collisions; a
+        // clean pass before that ends it (duplicate-heavy inputs)
         const int iters = (int)((mgs + 1u) >> 1);
         if (iters > 0) {
             const uint32_t q0 = 8u * lane;
@@ -741,19 +742,22 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 return sw_;
             };
             for (int it2 = 0; it2 < iters; it2++) {
-                cx(v[0], v[1], sv[0], sv[1]);
-                cx(v[2], v[3], sv[2], sv[3]);
-                cx(v[4], v[5], sv[4], sv[5]);
-                cx(v[6], v[7], sv[6], sv[7]);
-                cx(v[1], v[2], sv[1], sv[2]);
-                cx(v[3], v[4], sv[3], sv[4]);
-                cx(v[5], v[6], sv[5], sv[6]);
+                bool any = false;
+                any |= cx(v[0], v[1], sv[0], sv[1]);
+                any |= cx(v[2], v[3], sv[2], sv[3]);
+                any |= cx(v[4], v[5], sv[4], sv[5]);
+                any |= cx(v[6], v[7], sv[6], sv[7]);
+                any |= cx(v[1], v[2], sv[1], sv[2]);
+                any |= cx(v[3], v[4], sv[3], sv[4]);
+                any |= cx(v[5], v[6], sv[5], sv[6]);
                 const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
                 const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
                 const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                if (lane < 31 && sv[7] == ns && v[7] > nv) v[7] = nv;
-                if (lane > 0 && ps == sv[0] && pv > v[0]) v[0] = pv;
+                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                // equal keys never swap: stop early once a pass is clean
+                if (it2 + 1 < iters && !__any_sync(0xffffffffu, any)) break;
             }
             if (q0 < np) {
                 uint64_t *row = W.T + 9u * lane;
