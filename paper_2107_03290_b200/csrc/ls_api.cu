@@ -408,7 +408,8 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
     if (getenv("LS_DEBUG_STAGE")) {
         fprintf(stderr, "prof:");
         for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
-        fprintf(stderr, "\n");
+        fprintf(stderr, "\ntasks: warp %u cta256 %u cta128 %u windows %u large %u\n", c.ntask,
+                c.nctask, c.nctask2, c.nwin, c.nlarge);
     }
     if (c.status & STATUS_NAN) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
     if (c.status & STATUS_INTERNAL) { set_error("internal invariant violated (corrupt partition state)"); return LS_E_INTERNAL; }

@@ -94,7 +94,7 @@ template <int DT>
 __device__ __forceinline__ int root_leaf(uint64_t bits, const Root &R, double &xc) {
     xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
     const double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
-    return (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+    return (r < R.last) ? __double2int_rz(r) : R.Lm1;  // (NaN r: inf * 0 -> L-1)
 }
 
 // O6: p = F_A(x). `leaf` may point to shared or global memory.
@@ -102,7 +102,7 @@ template <int DT>
 __device__ __forceinline__ double predict(uint64_t bits, const Root &R, const double *leaf) {
     double xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
     double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
-    int l = (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+    const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;  // (NaN r: inf * 0 -> L-1)
     const double *q = leaf + 5 * l;
     double y = __fma_rn(q[0], __dsub_rn(xc, q[1]), q[2]);
     return __dadd_rn(clampd(y, q[3], q[4]), 0.0);
@@ -114,7 +114,7 @@ template <int DT>
 __device__ __forceinline__ double predict_ldg(uint64_t bits, const Root &R, const double *leaf) {
     double xc = clampd(xd<DT>(bits), R.xmin, R.xmax);
     double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
-    int l = (r < R.last) ? (int)__double2ll_rz(r) : R.Lm1;
+    const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;  // (NaN r: inf * 0 -> L-1)
     const double *q = leaf + 5 * l;
     double y = __fma_rn(__ldg(q), __dsub_rn(xc, __ldg(q + 1)), __ldg(q + 2));
     return __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
@@ -166,10 +166,13 @@ struct B0Search {
     }
 };
 
-// Alg.2 P:188-190 (R5): pos = clamp(floor((p - adj) * n), 0, n'-1)
-__device__ __forceinline__ uint32_t cs_pos(double p, double adj, double nd, double top) {
-    double v = floor(__dmul_rn(__dsub_rn(p, adj), nd));
-    return (uint32_t)__double2ll_rz(clampd(v, 0.0, top));
+// Alg.2 P:188-190 (R5): pos = clamp(floor((p - adj) * n), 0, n'-1). The
+// round-down conversion is floor; it saturates out-of-range values to the int
+// range (and NaN to 0), so the integer clamp gives the same pos as clamping
+// the double.
+__device__ __forceinline__ uint32_t cs_pos(double p, double adj, double nd, int top) {
+    const int v = __double2int_rd(__dmul_rn(__dsub_rn(p, adj), nd));
+    return (uint32_t)min(max(v, 0), top);
 }
 
 // ------------------------------------------------------------ control -----

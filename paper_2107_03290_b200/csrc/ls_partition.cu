@@ -481,7 +481,7 @@ __global__ void k_bucket_pos(const uint64_t *__restrict__ keys, uint64_t n, int 
         const uint32_t b0 = bucket0(p, F, f), b1 = bucket1(p, F2, f, b0);
         const uint64_t g = (uint64_t)b0 * f + b1;
         const double adj = __ddiv_rn((double)g, F2);
-        pos[i] = cs_pos(p, adj, nd, (double)(h1[g] - 1));
+        pos[i] = cs_pos(p, adj, nd, (int)(h1[g] - 1));
     }
 }
 

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 if (size_class(np, a.T_small) == SC_WINDOW && (uint32_t)i - h < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
-                    sl = h + cs_pos(p, adj, a.nd, (double)(np - 1u));
+                    sl = h + cs_pos(p, adj, a.nd, (int)(np - 1u));
                 }
                 // warp-aggregated: keys of equal slot (duplicates!) take one atomic
                 const uint32_t peers = __match_any_sync(__activemask(), sl);
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         __syncwarp();
         // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back)
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
-        const double top = (double)(np - 1u);
+        const int top = (int)(np - 1u);
         uint32_t code[WS_KPL];
 #pragma unroll
         for (int k = 0; k < WS_KPL; k++) {
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         if (tid == 0) S.nbig = S.ovf = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
-        const double top = (double)(np - 1u);
+        const int top = (int)(np - 1u);
         uint32_t code[CS_KPT];
 #pragma unroll
         for (int k = 0; k < CS_KPT; k++) {
