@@ -597,7 +597,6 @@ constexpr int WS_CTAS_PER_SM = 4;
 struct WsSlice {
     uint64_t T[WS_MAX + WS_MAX / 8];        // padded: position q at q + q/8
     uint32_t K[WS_MAX + 8];                 // pos histogram -> exclusive totals
-    uint16_t slot_of[WS_MAX];
     uint32_t big[32];                       // groups > 8 keys (their pos)
 };
 
@@ -709,33 +708,27 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 const uint32_t pos = code[k] & 0xffffu;
                 const uint32_t q = W.K[pos] + (code[k] >> 16);
                 T[q] = to_ord<DT>(key[k]);
-                W.slot_of[q] = (uint16_t)pos;
             }
         }
         __syncwarp();
-        // touch-up: odd-even transposition between equal-slot neighbours on
-        // 8 consecutive positions per lane; groups of <= mgs keys are sorted by
-        // mgs rounds (2 per iteration), none at all without collisions; a
-        // clean pass before that ends it (duplicate-heavy inputs)
+        // touch-up: odd-even transposition on 8 consecutive positions per
+        // lane. pos is monotone in the key (R15), so neighbours from different
+        // slots are already in order and never swap: every compare-exchange
+        // acts inside one collision group, which is sorted after as many
+        // rounds as it has keys (2 rounds per iteration; none without
+        // collisions; a clean pass ends it early on duplicate-heavy inputs).
+        // Groups > 8 are sorted again by the warp bitonic below.
         const int iters = (int)((mgs + 1u) >> 1);
         if (iters > 0) {
             const uint32_t q0 = 8u * lane;
             uint64_t v[8];
-            uint32_t sv[8];
             {
-                const uint2 s2 = reinterpret_cast<const uint2 *>(W.slot_of)[2 * lane];
-                const uint2 s3 = reinterpret_cast<const uint2 *>(W.slot_of)[2 * lane + 1];
-                const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
                 const uint64_t *row = W.T + 9u * lane;
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const bool in = q0 + q < np;
-                    v[q] = in ? row[q] : ~0ull;
-                    sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
-                }
+                for (int q = 0; q < 8; q++) v[q] = q0 + q < np ? row[q] : ~0ull;
             }
-            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
-                const bool sw_ = sx == sy && x > y;
+            auto cx = [](uint64_t &x, uint64_t &y) -> bool {
+                const bool sw_ = x > y;
                 const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
                 x = lo_;
                 y = hi_;
@@ -743,19 +736,17 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             };
             for (int it2 = 0; it2 < iters; it2++) {
                 bool any = false;
-                any |= cx(v[0], v[1], sv[0], sv[1]);
-                any |= cx(v[2], v[3], sv[2], sv[3]);
-                any |= cx(v[4], v[5], sv[4], sv[5]);
-                any |= cx(v[6], v[7], sv[6], sv[7]);
-                any |= cx(v[1], v[2], sv[1], sv[2]);
-                any |= cx(v[3], v[4], sv[3], sv[4]);
-                any |= cx(v[5], v[6], sv[5], sv[6]);
+                any |= cx(v[0], v[1]);
+                any |= cx(v[2], v[3]);
+                any |= cx(v[4], v[5]);
+                any |= cx(v[6], v[7]);
+                any |= cx(v[1], v[2]);
+                any |= cx(v[3], v[4]);
+                any |= cx(v[5], v[6]);
                 const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
-                const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
-                const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                if (lane < 31 && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && pv > v[0]) { v[0] = pv; any = true; }
                 // equal keys never swap: stop early once a pass is clean
                 if (it2 + 1 < iters && !__any_sync(0xffffffffu, any)) break;
             }
