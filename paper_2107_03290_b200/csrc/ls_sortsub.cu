@@ -590,6 +590,30 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
 // odd-even transposition between equal-slot neighbours, warp bitonic for
 // groups > 8) run in the warp's own shared-memory slice. A homogeneous
 // sub-bucket (first == last after sorting) is not written back.
+// Compare-exchange of two u64 keys with one predicate (setp + two selp per
+// half); returns 1 if they were swapped (only computed when `track`).
+__device__ __forceinline__ uint32_t cx_u64(uint64_t &x, uint64_t &y, bool track) {
+    uint64_t lo, hi;
+    uint32_t sw = 0;
+    if (track) {
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.gt.u64 p, %3, %4;\n\t"
+            "selp.b64 %0, %4, %3, p;\n\t"
+            "selp.b64 %1, %3, %4, p;\n\t"
+            "selp.u32 %2, 1, 0, p;\n\t}"
+            : "=l"(lo), "=l"(hi), "=r"(sw) : "l"(x), "l"(y));
+    } else {
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.gt.u64 p, %2, %3;\n\t"
+            "selp.b64 %0, %3, %2, p;\n\t"
+            "selp.b64 %1, %2, %3, p;\n\t}"
+            : "=l"(lo), "=l"(hi) : "l"(x), "l"(y));
+    }
+    x = lo;
+    y = hi;
+    return sw;
+}
+
 constexpr int WS_WARPS = 8;                 // warps per CTA
 constexpr int WS_KPL = (int)WS_MAX / 32;    // keys per lane (8)
 constexpr int WS_CTAS_PER_SM = 4;
@@ -727,29 +751,24 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 #pragma unroll
                 for (int q = 0; q < 8; q++) v[q] = q0 + q < np ? row[q] : ~0ull;
             }
-            auto cx = [](uint64_t &x, uint64_t &y) -> bool {
-                const bool sw_ = x > y;
-                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
-                x = lo_;
-                y = hi_;
-                return sw_;
-            };
-            for (int it2 = 0; it2 < iters; it2++) {
-                bool any = false;
-                any |= cx(v[0], v[1]);
-                any |= cx(v[2], v[3]);
-                any |= cx(v[4], v[5]);
-                any |= cx(v[6], v[7]);
-                any |= cx(v[1], v[2]);
-                any |= cx(v[3], v[4]);
-                any |= cx(v[5], v[6]);
+            // one pass = even pairs, odd pairs, the pair across lanes. Only
+            // the first pass reports whether anything moved (a clean first
+            // pass means every group is already in order: duplicate-heavy
+            // inputs); later passes skip that bookkeeping.
+            auto pass = [&](bool track) -> bool {
+                uint32_t moved = 0;
+#pragma unroll
+                for (int q = 0; q < 8; q += 2) moved |= cx_u64(v[q], v[q + 1], track);
+#pragma unroll
+                for (int q = 1; q < 7; q += 2) moved |= cx_u64(v[q], v[q + 1], track);
                 const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
-                if (lane < 31 && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && pv > v[0]) { v[0] = pv; any = true; }
-                // equal keys never swap: stop early once a pass is clean
-                if (it2 + 1 < iters && !__any_sync(0xffffffffu, any)) break;
-            }
+                if (lane < 31 && v[7] > nv) { v[7] = nv; moved = 1; }
+                if (lane > 0 && pv > v[0]) { v[0] = pv; moved = 1; }
+                return moved != 0;
+            };
+            if (__any_sync(0xffffffffu, pass(true)))
+                for (int it2 = 1; it2 < iters; it2++) pass(false);
             if (q0 < np) {
                 uint64_t *row = W.T + 9u * lane;
 #pragma unroll
