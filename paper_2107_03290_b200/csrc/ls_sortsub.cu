@@ -212,7 +212,7 @@ __device__ __forceinline__ double adj_of(uint32_t g, double F2, double rcp) {
 }
 
 // Sort c <= 32*NS ord values of a padded-T range by one warp in registers.
-template <int NS>
+template <int NS, bool PICK = true>
 __device__ __forceinline__ void warp_sort_T(PadT g, uint32_t c, int lane) {
     uint64_t v[NS];
 #pragma unroll
@@ -220,7 +220,7 @@ __device__ __forceinline__ void warp_sort_T(PadT g, uint32_t c, int lane) {
         const uint32_t i = 32u * s2 + lane;
         v[s2] = i < c ? g[i] : ~0ull;
     }
-    warp_sort_regs<NS>(v, lane);
+    warp_sort_regs<NS, uint64_t, PICK>(v, lane);
 #pragma unroll
     for (int s2 = 0; s2 < NS; s2++) {
         const uint32_t i = 32u * s2 + lane;
@@ -443,12 +443,10 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                     sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
                 }
             }
-            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
-                const bool sw_ = sx == sy && x > y;
-                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
-                x = lo_;
-                y = hi_;
-                return sw_;
+            // pos is monotone in the key (R15): neighbours of different slots
+            // are already in order, so the exchange needs no slot test
+            auto cx = [](uint64_t &x, uint64_t &y, uint32_t, uint32_t) -> bool {
+                return cx_u64(x, y, true) != 0;
             };
             for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
                 bool any = false;
@@ -463,8 +461,10 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
                 const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                (void)ns;
+                (void)ps;
+                if (lane < 31 && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && pv > v[0]) { v[0] = pv; any = true; }
                 if (!__any_sync(0xffffffffu, any)) break;
             }
             if (q0 < (uint32_t)span) {
@@ -590,30 +590,6 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
 // odd-even transposition between equal-slot neighbours, warp bitonic for
 // groups > 8) run in the warp's own shared-memory slice. A homogeneous
 // sub-bucket (first == last after sorting) is not written back.
-// Compare-exchange of two u64 keys with one predicate (setp + two selp per
-// half); returns 1 if they were swapped (only computed when `track`).
-__device__ __forceinline__ uint32_t cx_u64(uint64_t &x, uint64_t &y, bool track) {
-    uint64_t lo, hi;
-    uint32_t sw = 0;
-    if (track) {
-        asm("{\n\t.reg .pred p;\n\t"
-            "setp.gt.u64 p, %3, %4;\n\t"
-            "selp.b64 %0, %4, %3, p;\n\t"
-            "selp.b64 %1, %3, %4, p;\n\t"
-            "selp.u32 %2, 1, 0, p;\n\t}"
-            : "=l"(lo), "=l"(hi), "=r"(sw) : "l"(x), "l"(y));
-    } else {
-        asm("{\n\t.reg .pred p;\n\t"
-            "setp.gt.u64 p, %2, %3;\n\t"
-            "selp.b64 %0, %3, %2, p;\n\t"
-            "selp.b64 %1, %2, %3, p;\n\t}"
-            : "=l"(lo), "=l"(hi) : "l"(x), "l"(y));
-    }
-    x = lo;
-    y = hi;
-    return sw;
-}
-
 constexpr int WS_WARPS = 8;                 // warps per CTA
 constexpr int WS_KPL = (int)WS_MAX / 32;    // keys per lane (8)
 constexpr int WS_CTAS_PER_SM = 4;
@@ -776,7 +752,9 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             }
         }
         __syncwarp();
-        // groups > 8 keys: register bitonic by the whole warp
+        // groups > 8 keys: register bitonic by the whole warp (the plain
+        // select network: the single-predicate one costs the main path
+        // registers here)
         {
             const uint32_t nbl = W.K[WS_MAX + 7];
             for (uint32_t k = 0; k < nbl; k++) {
@@ -795,14 +773,14 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 if (__all_sync(0xffffffffu, same)) continue;
                 if (c <= 32u) {
                     uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
-                    warp_sort32(v1, lane);
+                    warp_sort32<false>(v1, lane);
                     if ((uint32_t)lane < c) T[base + lane] = v1;
                 } else if (c <= 64u) {
-                    warp_sort_T<2>(T + base, c, lane);
+                    warp_sort_T<2, false>(T + base, c, lane);
                 } else if (c <= 128u) {
-                    warp_sort_T<4>(T + base, c, lane);
+                    warp_sort_T<4, false>(T + base, c, lane);
                 } else {
-                    warp_sort_T<8>(T + base, c, lane);
+                    warp_sort_T<8, false>(T + base, c, lane);
                 }
             }
         }
@@ -1006,12 +984,10 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                         atomicOr(&S.mixed[sv[q] >> 5], 1u << (sv[q] & 31u));
                 }
             }
-            auto cx = [](uint64_t &x, uint64_t &y, uint32_t sx, uint32_t sy) -> bool {
-                const bool sw_ = sx == sy && x > y;
-                const uint64_t lo_ = sw_ ? y : x, hi_ = sw_ ? x : y;
-                x = lo_;
-                y = hi_;
-                return sw_;
+            // pos is monotone in the key (R15): neighbours of different slots
+            // are already in order, so the exchange needs no slot test
+            auto cx = [](uint64_t &x, uint64_t &y, uint32_t, uint32_t) -> bool {
+                return cx_u64(x, y, true) != 0;
             };
             for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
                 bool any = false;
@@ -1026,8 +1002,10 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
                 const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
                 const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                if (lane < 31 && sv[7] == ns && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && ps == sv[0] && pv > v[0]) { v[0] = pv; any = true; }
+                (void)ns;
+                (void)ps;
+                if (lane < 31 && v[7] > nv) { v[7] = nv; any = true; }
+                if (lane > 0 && pv > v[0]) { v[0] = pv; any = true; }
                 if (!__any_sync(0xffffffffu, any)) break;
             }
             if (q0 < np) {
