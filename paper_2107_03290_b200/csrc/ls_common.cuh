@@ -120,6 +120,19 @@ __device__ __forceinline__ double predict_ldg(uint64_t bits, const Root &R, cons
     return __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
 }
 
+// predict_ldg for a key known to lie in [xmin, xmax] (the root clamp is the
+// identity there), and the sub-bucket g = b0 * f + b1 that the clamped keys
+// (x < xmin or x > xmax) share with xmin / xmax themselves.
+template <int DT>
+__device__ __forceinline__ double predict_ldg_inner(uint64_t bits, const Root &R, const double *leaf) {
+    const double xc = xd<DT>(bits);
+    double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;
+    const double *q = leaf + 5 * l;
+    double y = __fma_rn(__ldg(q), __dsub_rn(xc, __ldg(q + 1)), __ldg(q + 2));
+    return __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
+}
+
 // O7 / Alg.1 P:107 (R1)
 __device__ __forceinline__ uint32_t bucket0(double p, double F, int f) {
     long long b = __double2ll_rz(__dmul_rn(p, F));
@@ -130,6 +143,18 @@ __device__ __forceinline__ uint32_t bucket1(double p, double F2, int f, uint32_t
     long long b = __double2ll_rz(__dmul_rn(p, F2)) - (long long)parent * f;
     b = b < 0 ? 0 : b;
     return (uint32_t)(b > f - 1 ? f - 1 : b);
+}
+
+// Sub-bucket of the prediction at the double xc (a root-clamped key).
+__device__ __forceinline__ uint32_t sub_bucket_at(double xc, const Root &R, const double *leaf,
+                                                  double F, double F2, int f) {
+    double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;
+    const double *q = leaf + 5 * l;
+    const double y = __fma_rn(q[0], __dsub_rn(xc, q[1]), q[2]);
+    const double p = __dadd_rn(clampd(y, q[3], q[4]), 0.0);
+    const uint32_t b0 = bucket0(p, F, f);
+    return b0 * (uint32_t)f + bucket1(p, F2, f, b0);
 }
 
 // Grid cell of a key for the b0 search (monotone in ord).

@@ -594,9 +594,9 @@ constexpr int WS_WARPS = 8;                 // warps per CTA
 constexpr int WS_KPL = (int)WS_MAX / 32;    // keys per lane (8)
 constexpr int WS_CTAS_PER_SM = 4;
 
-struct WsSlice {
+struct alignas(16) WsSlice {
     uint64_t T[WS_MAX + WS_MAX / 8];        // padded: position q at q + q/8
-    uint32_t K[WS_MAX + 8];                 // pos histogram -> exclusive totals
+    alignas(16) uint32_t K[WS_MAX + 8];     // pos histogram -> exclusive totals
     uint32_t big[32];                       // groups > 8 keys (their pos)
 };
 
@@ -612,6 +612,8 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     __syncthreads();
     const uint32_t ntask = min(a.ctl->ntask, a.task_cap);
     const Root R = load_root(a.M);
+    const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
+    const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t nw = gridDim.x * WS_WARPS;
     uint32_t r_small = 0, r_smallk = 0, r_h1 = 0, r_h1k = 0, r_maxg = 0;
     uint4 nxt = blockIdx.x * WS_WARPS + warp < ntask ? a.tasks[blockIdx.x * WS_WARPS + warp]
@@ -621,11 +623,9 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         const uint32_t st = task.x, np = task.y, g = task.z;
         // keys (coalesced), and the next task's descriptor, in flight together
         uint64_t key[WS_KPL];
+        uint64_t *const gl = a.A + st + lane;  // key 32k + lane at gl[32k]
 #pragma unroll
-        for (int k = 0; k < WS_KPL; k++) {
-            const uint32_t i = 32u * k + lane;
-            key[k] = i < np ? a.A[st + i] : 0ull;
-        }
+        for (int k = 0; k < WS_KPL; k++) key[k] = 32u * k + lane < np ? gl[32 * k] : 0ull;
         if (t + nw < ntask) nxt = a.tasks[t + nw];
         // homogeneous sub-bucket (all keys equal): nothing to sort or store
         {
@@ -643,21 +643,36 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 continue;
             }
         }
-        for (uint32_t i = lane; i <= np; i += 32) W.K[i] = 0;
+        for (uint32_t i = 4 * lane; i <= np; i += 128)
+            *reinterpret_cast<uint4 *>(&W.K[i]) = make_uint4(0, 0, 0, 0);
         __syncwarp();
-        // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back)
+        // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back).
+        // Only the sub-buckets of xmin and xmax can hold keys outside
+        // [xmin, xmax]; elsewhere the root clamp is skipped.
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
         uint32_t code[WS_KPL];
+        if (g != g_lo && g != g_hi) {
 #pragma unroll
-        for (int k = 0; k < WS_KPL; k++) {
-            const uint32_t i = 32u * k + lane;
-            code[k] = BS_NONE;
-            if (i < np) {
-                const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
-                const uint32_t pos = cs_pos(p, adj, a.nd, top);
-                const uint32_t r = atomicAdd(&W.K[pos], 1u);
-                code[k] = pos | (r << 16);
+            for (int k = 0; k < WS_KPL; k++) {
+                code[k] = BS_NONE;
+                if (32u * k + lane < np) {
+                    const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
+                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                    code[k] = pos | (r << 16);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < WS_KPL; k++) {
+                code[k] = BS_NONE;
+                if (32u * k + lane < np) {
+                    const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
+                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                    code[k] = pos | (r << 16);
+                }
             }
         }
         __syncwarp();
@@ -787,11 +802,10 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         __syncwarp();
         // homogeneous iff first == last of the sorted sub-bucket
         if (T[0] != T[np - 1u]) {
+            const uint64_t *tl = W.T + lane + (lane >> 3);  // T[32k + lane] at tl[36k]
 #pragma unroll
-            for (int k = 0; k < WS_KPL; k++) {
-                const uint32_t i = 32u * k + lane;
-                if (i < np) a.A[st + i] = from_ord<DT>(T[i]);
-            }
+            for (int k = 0; k < WS_KPL; k++)
+                if (32u * k + lane < np) gl[32 * k] = from_ord<DT>(tl[36 * k]);
             r_small++;
             r_smallk += np;
         } else {
