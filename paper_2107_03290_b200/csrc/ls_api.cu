@@ -41,7 +41,7 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -104,6 +104,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.tasks = take((size_t)l.task_cap * 16);
     l.ctasks = take((size_t)l.task_cap * 16);
     l.ctasks2 = take((size_t)l.task_cap * 16);
+    l.ctasks3 = take((size_t)l.task_cap * 16);
     l.large = take((size_t)l.lcap * 4);
     l.lstart = take((size_t)l.lcap * 1024 * 4);
     l.lcur = take((size_t)l.lcap * 1024 * 4);
@@ -164,6 +165,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.tasks = (uint4 *)(w + l.tasks);
     a.ctasks = (uint4 *)(w + l.ctasks);
     a.ctasks2 = (uint4 *)(w + l.ctasks2);
+    a.ctasks3 = (uint4 *)(w + l.ctasks3);
     a.large = (uint32_t *)(w + l.large);
     a.lcap = l.lcap;
     a.pcap = l.pcap;
@@ -345,7 +347,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
     launch_bucketsort(a, dt, st);
-    launches += 5;
+    launches += 6;
     tm.mark(LS_PHASE_BUCKETSORT);
     launch_big_minmax(a, dt, st);
     launches++;
@@ -408,8 +410,8 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
     if (getenv("LS_DEBUG_STAGE")) {
         fprintf(stderr, "prof:");
         for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
-        fprintf(stderr, "\ntasks: warp %u cta256 %u cta128 %u windows %u large %u\n", c.ntask,
-                c.nctask, c.nctask2, c.nwin, c.nlarge);
+        fprintf(stderr, "\ntasks: warp %u cta4096 %u cta2048 %u cta1024 %u windows %u large %u\n",
+                c.ntask, c.nctask, c.nctask2, c.nctask3, c.nwin, c.nlarge);
     }
     if (c.status & STATUS_NAN) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
     if (c.status & STATUS_INTERNAL) { set_error("internal invariant violated (corrupt partition state)"); return LS_E_INTERNAL; }

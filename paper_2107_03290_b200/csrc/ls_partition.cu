@@ -28,7 +28,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
-        ctl->ntask = ctl->nctask = ctl->nctask2 = 0;
+        ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = 0;
         ctl->nlarge = ctl->npiece = 0;
         ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
@@ -375,30 +375,32 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     // warp / CTA sorts become task lists (compacted per block: one global
     // atomic per level-0 bucket and class)
     {
-        __shared__ uint32_t wcnt[3][32], wbase[3];
+        __shared__ uint32_t wcnt[4][32], wbase[4];
         const int lane = tid & 31, w = tid >> 5;
-        uint32_t m[3];
+        uint32_t m[4];
         m[0] = __ballot_sync(0xffffffffu, sc == SC_WARP);
         m[1] = __ballot_sync(0xffffffffu, sc == SC_CTA);
         m[2] = __ballot_sync(0xffffffffu, sc == SC_CTAM);
+        m[3] = __ballot_sync(0xffffffffu, sc == SC_CTAL);
         if (lane == 0)
-            for (int q = 0; q < 3; q++) wcnt[q][w] = __popc(m[q]);
+            for (int q = 0; q < 4; q++) wcnt[q][w] = __popc(m[q]);
         __syncthreads();
-        if (tid < 3) {
+        if (tid < 4) {
             uint32_t tot = 0;
             for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
                 const uint32_t t = wcnt[tid][q];
                 wcnt[tid][q] = tot;
                 tot += t;
             }
-            uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask : &a.ctl->nctask2;
+            uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask
+                          : tid == 2 ? &a.ctl->nctask2 : &a.ctl->nctask3;
             wbase[tid] = tot ? atomicAdd(ctr, tot) : 0u;
         }
         __syncthreads();
-        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : -1;
+        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : sc == SC_CTAL ? 3 : -1;
         if (c2 >= 0) {
             const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m[c2] & ((1u << lane) - 1u));
-            uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : a.ctasks2;
+            uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : c2 == 2 ? a.ctasks2 : a.ctasks3;
             if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, 0u);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }

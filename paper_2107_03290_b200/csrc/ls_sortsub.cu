@@ -838,7 +838,6 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 // counting sort (K in shared memory), placement into padded T, odd-even
 // touch-up on 8 consecutive positions per thread (groups straddling two warps
 // and groups > 8 are sorted by warps), homogeneity = first == last, store.
-constexpr int CS_KPT = 16;  // keys per thread; capacity = 16 x threads
 
 template <int CAP>
 struct CsSmem {
@@ -848,13 +847,13 @@ struct CsSmem {
     uint16_t slot_of[CAP];
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
-    uint32_t nbig, ovf;
+    uint32_t nbig, ovf, mgs;
     unsigned long long st[5];
 };
 
 // CS_THREADS = 256 for 2049..4096 keys (3 CTAs/SM), 128 for 257..2048 (6 CTAs/SM:
 // more tasks in flight where a task is short and latency-bound).
-template <int DT, int CS_THREADS, int CS_CTAS_PER_SM>
+template <int DT, int CS_THREADS, int CS_KPT, int CS_CTAS_PER_SM>
 __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, const uint4 *list,
                                                                      const uint32_t *count) {
     if (a.ctl->status) return;
@@ -865,15 +864,20 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
     const PadT T{S.T, 0u};
     const uint32_t ntask = min(*count, a.task_cap);
     const Root R = load_root(a.M);
+    const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
+    const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
     if (tid < 5) S.st[tid] = 0;
     for (uint32_t t = blockIdx.x; t < ntask; t += gridDim.x) {
         const uint4 task = list[t];
         const uint32_t st = task.x, np = task.y, g = task.z;
+        // every per-key loop stops (block-uniform branch) after the
+        // kn = ceil(np / CS_THREADS) rows that hold keys
+        const int kn = (int)((np + CS_THREADS - 1) / CS_THREADS);
         uint64_t key[CS_KPT];
+        uint64_t *const gl = a.A + st + tid;  // key k * CS_THREADS + tid at gl[k * CS_THREADS]
 #pragma unroll
         for (int k = 0; k < CS_KPT; k++) {
-            const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
-            key[k] = i < np ? a.A[st + i] : 0ull;
+            key[k] = (uint32_t)(k * CS_THREADS + tid) < np ? gl[k * CS_THREADS] : 0ull;
         }
         // homogeneous sub-bucket (all keys equal): nothing to sort or store
         {
@@ -894,21 +898,32 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
-        for (uint32_t i = tid; i < (np + 31) / 32; i += CS_THREADS) S.mixed[i] = 0;
-        if (tid == 0) S.nbig = S.ovf = 0;
+        if (tid == 0) S.nbig = S.ovf = S.mgs = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
         uint32_t code[CS_KPT];
+        if (g != g_lo && g != g_hi) {  // keys inside [xmin, xmax]: no root clamp
 #pragma unroll
-        for (int k = 0; k < CS_KPT; k++) {
-            const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
-            code[k] = BS_NONE;
-            if (i < np) {
-                const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
-                const uint32_t pos = cs_pos(p, adj, a.nd, top);
-                const uint32_t r = atomicAdd(&S.K[pos], 1u);
-                code[k] = pos | (r << 12);
+            for (int k = 0; k < CS_KPT; k++) {
+                code[k] = BS_NONE;
+                if ((uint32_t)(k * CS_THREADS + tid) < np) {
+                    const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
+                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t r = atomicAdd(&S.K[pos], 1u);
+                    code[k] = pos | (r << 12);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < CS_KPT; k++) {
+                code[k] = BS_NONE;
+                if ((uint32_t)(k * CS_THREADS + tid) < np) {
+                    const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
+                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t r = atomicAdd(&S.K[pos], 1u);
+                    code[k] = pos | (r << 12);
+                }
             }
         }
         __syncthreads();
@@ -917,10 +932,11 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         {
             const uint32_t per = (np + CS_THREADS) / CS_THREADS;
             const uint32_t b0 = per * tid, b1 = min(b0 + per, np + 1u);
-            uint32_t sum = 0, mg = 0;
+            uint32_t sum = 0, mg = 0, mgs = 0;
             for (uint32_t idx = b0; idx < b1; idx++) {
                 const uint32_t c = idx < np ? S.K[idx] : 0u;
                 mg = c > mg ? c : mg;
+                mgs = (c <= BS_RANKMAX && c > mgs) ? c : mgs;
                 if (c > BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
@@ -928,7 +944,9 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 sum += c;
             }
             mg = __reduce_max_sync(0xffffffffu, mg);
+            mgs = __reduce_max_sync(0xffffffffu, mgs);
             if (lane == 0 && mg > 1u) atomicMax(&S.st[4], (unsigned long long)mg);
+            if (lane == 0 && mgs > 1u) atomicMax(&S.mgs, mgs);
             const uint32_t incl = warp_incl_scan(sum);
             if (lane == 31) S.wsum[warp] = incl;
             __syncthreads();
@@ -945,7 +963,11 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         __syncthreads();
-        // placement
+        // placement; with groups > 8 listed, clear their
+        // mixed-value flags (set in the touch-up, read by the group sorts)
+        const bool has_big = S.nbig > 0;
+        if (has_big)
+            for (uint32_t i = tid; i < (np + 31) / 32; i += CS_THREADS) S.mixed[i] = 0;
 #pragma unroll
         for (int k = 0; k < CS_KPT; k++) {
             if (code[k] != BS_NONE) {
@@ -956,80 +978,65 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         __syncthreads();
-        // touch-up: odd-even between equal-slot neighbours, 16 consecutive
-        // positions per thread as two rows of 8 (the second only if np > 2048)
-        for (int half = 0; half < (np > 8u * CS_THREADS ? 2 : 1); half++) {
+        // touch-up: odd-even transposition, 16 consecutive positions per
+        // thread as two rows of 8 (the second only if np > 2048). pos is
+        // monotone in the key (R15), so neighbours of different slots are in
+        // order already and never swap; groups of <= mgs keys need mgs rounds
+        // (2 per pass), and a clean first pass ends it (duplicates).
+        const int iters = (int)((S.mgs + 1u) >> 1);
+        for (int half = 0; half < (CS_KPT > 8 && np > 8u * CS_THREADS ? 2 : 1); half++) {
             const uint32_t row_i = (uint32_t)(half * CS_THREADS + tid);  // row of 8 positions
             const uint32_t q0 = 8u * row_i;
-            uint64_t v[8];
-            uint32_t sv[8];
-            {
+            if (has_big && q0 < np) {
+                // mixed-group flags: equal-slot neighbours with different keys
+                // (the pair across two rows is checked from the row on the left)
+                const uint64_t *row = S.T + 9u * row_i;
                 const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i];
                 const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i + 1];
                 const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
-                const uint64_t *row = S.T + 9u * row_i;
+                const uint32_t last = min(8u, np - q0);  // positions of this row
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                    const bool in = q0 + q < np;
-                    v[q] = in ? row[q] : ~0ull;
-                    sv[q] = in ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
-                }
-            }
-            // mixed-group flags (adjacent equal-slot pairs with different keys;
-            // the pair across two rows is checked from the row on the left,
-            // using shared memory at warp boundaries)
-            {
-                uint64_t nv0 = __shfl_down_sync(0xffffffffu, v[0], 1);
-                uint32_t ns0 = __shfl_down_sync(0xffffffffu, sv[0], 1);
-                if (lane == 31) {
-                    const uint32_t qn = q0 + 8u;
-                    if (qn < np) {
-                        nv0 = S.T[9u * (row_i + 1u)];
-                        ns0 = S.slot_of[qn];
-                    } else {
-                        ns0 = 0xfffffu;
+                    const uint32_t qn = q0 + q + 1;
+                    if ((uint32_t)q < last && qn < np) {
+                        const uint32_t sq = (sw[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+                        const uint32_t sn = q < 7 ? (sw[(q + 1) >> 1] >> (16 * ((q + 1) & 1))) & 0xffffu
+                                                  : (uint32_t)S.slot_of[qn];
+                        const uint64_t y = q < 7 ? row[q + 1] : S.T[9u * (row_i + 1u)];
+                        if (sq == sn && row[q] != y) atomicOr(&S.mixed[sq >> 5], 1u << (sq & 31u));
                     }
                 }
+            }
+            if (iters > 0) {
+                uint64_t v[8];
+                {
+                    const uint64_t *row = S.T + 9u * row_i;
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const uint64_t y = q < 7 ? v[q + 1] : nv0;
-                    const uint32_t sy = q < 7 ? sv[q + 1] : ns0;
-                    if (sv[q] < 0x10000u && sv[q] == sy && v[q] != y)
-                        atomicOr(&S.mixed[sv[q] >> 5], 1u << (sv[q] & 31u));
+                    for (int q = 0; q < 8; q++) v[q] = q0 + q < np ? row[q] : ~0ull;
+                }
+                auto pass = [&](bool track) -> bool {
+                    uint32_t moved = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2) moved |= cx_u64(v[q], v[q + 1], track);
+#pragma unroll
+                    for (int q = 1; q < 7; q += 2) moved |= cx_u64(v[q], v[q + 1], track);
+                    const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
+                    const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
+                    if (lane < 31 && v[7] > nv) { v[7] = nv; moved = 1; }
+                    if (lane > 0 && pv > v[0]) { v[0] = pv; moved = 1; }
+                    return moved != 0;
+                };
+                if (__any_sync(0xffffffffu, pass(true)))
+                    for (int it2 = 1; it2 < iters; it2++) pass(false);
+                if (q0 < np) {
+                    uint64_t *row = S.T + 9u * row_i;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) row[q] = v[q];
                 }
             }
-            // pos is monotone in the key (R15): neighbours of different slots
-            // are already in order, so the exchange needs no slot test
-            auto cx = [](uint64_t &x, uint64_t &y, uint32_t, uint32_t) -> bool {
-                return cx_u64(x, y, true) != 0;
-            };
-            for (int round = 0; round < (int)BS_RANKMAX; round += 2) {
-                bool any = false;
-                any |= cx(v[0], v[1], sv[0], sv[1]);
-                any |= cx(v[2], v[3], sv[2], sv[3]);
-                any |= cx(v[4], v[5], sv[4], sv[5]);
-                any |= cx(v[6], v[7], sv[6], sv[7]);
-                any |= cx(v[1], v[2], sv[1], sv[2]);
-                any |= cx(v[3], v[4], sv[3], sv[4]);
-                any |= cx(v[5], v[6], sv[5], sv[6]);
-                const uint64_t nv = __shfl_down_sync(0xffffffffu, v[0], 1);
-                const uint32_t ns = __shfl_down_sync(0xffffffffu, sv[0], 1);
-                const uint64_t pv = __shfl_up_sync(0xffffffffu, v[7], 1);
-                const uint32_t ps = __shfl_up_sync(0xffffffffu, sv[7], 1);
-                (void)ns;
-                (void)ps;
-                if (lane < 31 && v[7] > nv) { v[7] = nv; any = true; }
-                if (lane > 0 && pv > v[0]) { v[0] = pv; any = true; }
-                if (!__any_sync(0xffffffffu, any)) break;
-            }
-            if (q0 < np) {
-                uint64_t *row = S.T + 9u * row_i;
-#pragma unroll
-                for (int q = 0; q < 8; q++) row[q] = v[q];
-            }
             // a small group straddling two warps' 256-position ranges
-            if (lane == 0 && row_i > 0 && q0 < np && sv[0] < 0x10000u && S.slot_of[q0 - 1] == sv[0]) {
-                const uint32_t sl = sv[0], c = S.K[sl + 1] - S.K[sl];
+            if (lane == 0 && row_i > 0 && q0 < np && S.slot_of[q0 - 1] == S.slot_of[q0]) {
+                const uint32_t sl = S.slot_of[q0], c = S.K[sl + 1] - S.K[sl];
                 if (c <= BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = sl; else S.ovf = 1;
@@ -1049,7 +1056,6 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     sl = k - nb;
                     if (S.K[sl + 1] - S.K[sl] < 2u) continue;
                 }
-                if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
                 if (c <= BS_RANKMAX) {
                     if (lane == 0) {
@@ -1065,6 +1071,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     }
                     continue;
                 }
+                if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
                 if (c <= 32u) {
                     uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
                     warp_sort32(v1, lane);
@@ -1084,10 +1091,11 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         // homogeneous iff first == last of the sorted sub-bucket
         const bool homog = T[0] == T[np - 1u];
         if (!homog) {
+            // T[k * CS_THREADS + tid] at tl[k * CS_THREADS * 9 / 8] (CS_THREADS % 8 == 0)
+            const uint64_t *tl = S.T + tid + (tid >> 3);
 #pragma unroll
             for (int k = 0; k < CS_KPT; k++) {
-                const uint32_t i = (uint32_t)(k * CS_THREADS + tid);
-                if (i < np) a.A[st + i] = from_ord<DT>(T[i]);
+                if ((uint32_t)(k * CS_THREADS + tid) < np) gl[k * CS_THREADS] = from_ord<DT>(tl[k * CS_THREADS * 9 / 8]);
             }
         }
         if (tid == 0) {
@@ -1460,17 +1468,17 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
 }
 
 // -------------------------------------------------------------- launchers --
-template <int NT, int PER_SM>
+template <int NT, int KPT, int PER_SM>
 static void launch_ctasort(const Args &a, int dtype, cudaStream_t st, const uint4 *list,
                            const uint32_t *count, int sms) {
-    const size_t sm = sizeof(CsSmem<NT * CS_KPT>);
+    const size_t sm = sizeof(CsSmem<NT * KPT>);
     const int g = sms * PER_SM;
     if (dtype == DT_F64) {
-        cudaFuncSetAttribute(k_ctasort<DT_F64, NT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_ctasort<DT_F64, NT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
+        cudaFuncSetAttribute(k_ctasort<DT_F64, NT, KPT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_ctasort<DT_F64, NT, KPT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
     } else {
-        cudaFuncSetAttribute(k_ctasort<DT_U64, NT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_ctasort<DT_U64, NT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
+        cudaFuncSetAttribute(k_ctasort<DT_U64, NT, KPT, PER_SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_ctasort<DT_U64, NT, KPT, PER_SM><<<g, NT, sm, st>>>(a, list, count);
     }
 }
 
@@ -1482,8 +1490,9 @@ void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
         const int g = sms * WS_CTAS_PER_SM;
         if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
         else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
-        launch_ctasort<256, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
-        launch_ctasort<128, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
+        launch_ctasort<256, 16, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
+        launch_ctasort<128, 16, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
+        launch_ctasort<128, 8, 8>(a, dtype, st, a.ctasks3, &a.ctl->nctask3, sms);
     }
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
