@@ -70,7 +70,7 @@ __device__ __forceinline__ void bitonic(uint64_t *g, int c, int lane, int lanes)
 }
 
 // Bitonic over an indexable view (same network as bitonic()).
-template <class V>
+template <class V, bool BLOCK = false>
 __device__ __forceinline__ void bitonic_view(V g, int c, int lane, int lanes) {
     int P = 1, lg = 0;
     while (P < c) { P <<= 1; lg++; }
@@ -86,7 +86,7 @@ __device__ __forceinline__ void bitonic_view(V g, int c, int lane, int lanes) {
             const int lo = blk * k + p, hi = blk * k + k - 1 - p;
             if (hi < c) cs(lo, hi);
         }
-        __syncwarp();
+        if (BLOCK) __syncthreads(); else __syncwarp();
         for (int lj = lk - 2; lj >= 0; lj--) {
             const int j = 1 << lj;
             for (int i = lane; i < halfP; i += lanes) {
@@ -94,7 +94,7 @@ __device__ __forceinline__ void bitonic_view(V g, int c, int lane, int lanes) {
                 const int lo = blk * 2 * j + p, hi = lo + j;
                 if (hi < c) cs(lo, hi);
             }
-            __syncwarp();
+            if (BLOCK) __syncthreads(); else __syncwarp();
         }
     }
 }
@@ -847,7 +847,7 @@ struct CsSmem {
     uint16_t slot_of[CAP];
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
-    uint32_t nbig, ovf, mgs;
+    uint32_t nbig, ovf, mgs, mgx;   // mgx: a group > 8 keys outside slot n'-1
     unsigned long long st[5];
 };
 
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
-        if (tid == 0) S.nbig = S.ovf = S.mgs = 0;
+        if (tid == 0) S.nbig = S.ovf = S.mgs = S.mgx = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
@@ -940,6 +940,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 if (c > BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
+                    if (idx != np - 1u) S.mgx = 1u;  // a big group other than R5's end pile-up
                 }
                 sum += c;
             }
@@ -963,9 +964,13 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         __syncthreads();
-        // placement; with groups > 8 listed, clear their
-        // mixed-value flags (set in the touch-up, read by the group sorts)
-        const bool has_big = S.nbig > 0;
+        // placement. With a group of > 8 keys in any slot but the
+        // last (duplicate-heavy inputs) all threads flag the mixed-value
+        // groups in the touch-up, so that the group sorts skip one-value
+        // groups without a serial scan. A big group in slot n'-1 alone is the
+        // pile-up of R5's clamp when n' < n / f^2 (smooth inputs at n ~ 10^9):
+        // its warp checks it.
+        const bool has_big = S.mgx != 0;
         if (has_big)
             for (uint32_t i = tid; i < (np + 31) / 32; i += CS_THREADS) S.mixed[i] = 0;
 #pragma unroll
@@ -987,32 +992,42 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         for (int half = 0; half < (CS_KPT > 8 && np > 8u * CS_THREADS ? 2 : 1); half++) {
             const uint32_t row_i = (uint32_t)(half * CS_THREADS + tid);  // row of 8 positions
             const uint32_t q0 = 8u * row_i;
-            if (has_big && q0 < np) {
-                // mixed-group flags: equal-slot neighbours with different keys
-                // (the pair across two rows is checked from the row on the left)
-                const uint64_t *row = S.T + 9u * row_i;
-                const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i];
-                const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i + 1];
-                const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
-                const uint32_t last = min(8u, np - q0);  // positions of this row
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const uint32_t qn = q0 + q + 1;
-                    if ((uint32_t)q < last && qn < np) {
-                        const uint32_t sq = (sw[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-                        const uint32_t sn = q < 7 ? (sw[(q + 1) >> 1] >> (16 * ((q + 1) & 1))) & 0xffffu
-                                                  : (uint32_t)S.slot_of[qn];
-                        const uint64_t y = q < 7 ? row[q + 1] : S.T[9u * (row_i + 1u)];
-                        if (sq == sn && row[q] != y) atomicOr(&S.mixed[sq >> 5], 1u << (sq & 31u));
-                    }
-                }
-            }
-            if (iters > 0) {
+            if (iters > 0 || has_big) {
                 uint64_t v[8];
                 {
                     const uint64_t *row = S.T + 9u * row_i;
 #pragma unroll
                     for (int q = 0; q < 8; q++) v[q] = q0 + q < np ? row[q] : ~0ull;
+                }
+                if (has_big) {
+                    // mixed-group flags: equal-slot neighbours with different
+                    // keys (the pair across two rows from the row on the left;
+                    // shared memory at warp boundaries)
+                    const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i];
+                    const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i + 1];
+                    const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
+                    uint32_t sv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        sv[q] = q0 + q < np ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
+                    uint64_t nv0 = __shfl_down_sync(0xffffffffu, v[0], 1);
+                    uint32_t ns0 = __shfl_down_sync(0xffffffffu, sv[0], 1);
+                    if (lane == 31) {
+                        const uint32_t qn = q0 + 8u;
+                        if (qn < np) {
+                            nv0 = S.T[9u * (row_i + 1u)];
+                            ns0 = S.slot_of[qn];
+                        } else {
+                            ns0 = 0xfffffu;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const uint64_t y = q < 7 ? v[q + 1] : nv0;
+                        const uint32_t sy = q < 7 ? sv[q + 1] : ns0;
+                        if (sv[q] < 0x10000u && sv[q] == sy && v[q] != y)
+                            atomicOr(&S.mixed[sv[q] >> 5], 1u << (sv[q] & 31u));
+                    }
                 }
                 auto pass = [&](bool track) -> bool {
                     uint32_t moved = 0;
@@ -1026,12 +1041,16 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     if (lane > 0 && pv > v[0]) { v[0] = pv; moved = 1; }
                     return moved != 0;
                 };
-                if (__any_sync(0xffffffffu, pass(true)))
-                    for (int it2 = 1; it2 < iters; it2++) pass(false);
-                if (q0 < np) {
-                    uint64_t *row = S.T + 9u * row_i;
+                if (iters > 0) {
+                    // (every pass votes: duplicate-heavy sub-buckets, the
+                    // usual CTA case, mostly converge early)
+                    for (int it2 = 0; it2 < iters; it2++)
+                        if (!__any_sync(0xffffffffu, pass(true))) break;
+                    if (q0 < np) {
+                        uint64_t *row = S.T + 9u * row_i;
 #pragma unroll
-                    for (int q = 0; q < 8; q++) row[q] = v[q];
+                        for (int q = 0; q < 8; q++) row[q] = v[q];
+                    }
                 }
             }
             // a small group straddling two warps' 256-position ranges
@@ -1057,6 +1076,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     if (S.K[sl + 1] - S.K[sl] < 2u) continue;
                 }
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
+                if (c > 256u && k < nb) continue;  // the whole CTA sorts it below
                 if (c <= BS_RANKMAX) {
                     if (lane == 0) {
                         for (uint32_t x = 1; x < c; x++) {
@@ -1071,7 +1091,13 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     }
                     continue;
                 }
-                if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
+                if (has_big) {
+                    if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
+                } else {
+                    bool same = true;
+                    for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
+                    if (__all_sync(0xffffffffu, same)) continue;
+                }
                 if (c <= 32u) {
                     uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
                     warp_sort32(v1, lane);
@@ -1085,6 +1111,22 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 } else {
                     bitonic_view(T + base, (int)c, lane, 32);
                 }
+            }
+            __syncthreads();
+            // listed groups of > 256 keys (duplicate-heavy inputs): shared-
+            // memory bitonic by all threads, one group at a time
+            for (uint32_t k = 0; k < nb; k++) {
+                const uint32_t sl = S.big[k];
+                const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
+                if (c <= 256u) continue;
+                if (has_big) {
+                    if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
+                } else {
+                    bool diff = false;
+                    for (uint32_t q = tid; q < c; q += CS_THREADS) diff |= (T[base + q] != T[base]);
+                    if (!__syncthreads_or(diff)) continue;
+                }
+                bitonic_view<PadT, true>(T + base, (int)c, tid, CS_THREADS);
             }
         }
         __syncthreads();
