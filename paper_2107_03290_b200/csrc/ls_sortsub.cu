@@ -1187,6 +1187,7 @@ constexpr int BIG_SORT_CAP = 8192;     // keys sorted in shared memory by one CT
 constexpr int BIG_CHUNK = BIG_SORT_CAP / 2;
 constexpr int BIG_MAXWIN = 1024;       // windows classified per round
 constexpr int BIG_MAXBLK = 64;         // pieces in (BIG_CHUNK, BIG_SORT_CAP] per item
+constexpr int BIG_MAXWBIG = 16;        // pieces of 257..BIG_CHUNK keys per window (CTA-sorted)
 
 // ord min/max of level-0 big items, one 64K-key chunk per work entry
 // (classify wrote the chunk list), so a multi-million-key homogeneous
@@ -1275,8 +1276,9 @@ struct BigSmem {
     uint32_t start[BIG_DIGITS], end[BIG_DIGITS];
     uint32_t wlo[BIG_MAXWIN], whi[BIG_MAXWIN];
     uint32_t blk[BIG_MAXBLK];
+    uint32_t wbig[BIG_MAXWBIG];             // window pieces of 257..BIG_CHUNK keys
     uint32_t tmp[36];
-    uint32_t item, nblk;
+    uint32_t item, nblk, nwbig;
     unsigned long long red[64];
 };
 
@@ -1453,6 +1455,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                         bulk_g2s((char *)S.sk + o, (const char *)(Yb + h0) + o,
                                  bytes - o < 32768u ? bytes - o : 32768u, &S.mbar);
                 }
+                if (tid == 0) S.nwbig = 0;
                 BG_PROF(5);
                 mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
@@ -1483,11 +1486,25 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
                         warp_sort_keys<DT, 4>(g, pc, lane);
                     } else if (pc <= 256) {
                         warp_sort_keys<DT, 8>(g, pc, lane);
-                    } else if (pc <= BIG_CHUNK) {
-                        bitonic<DT, false>(g, (int)pc, lane, 32);
+                    } else {  // listed for the whole CTA below (one warp would hold up the window)
+                        uint32_t k = 0;
+                        if (lane == 0) k = atomicAdd(&S.nwbig, 1u);
+                        k = __shfl_sync(0xffffffffu, k, 0);
+                        if (k < BIG_MAXWBIG) {
+                            if (lane == 0) S.wbig[k] = d;
+                        } else {
+                            bitonic<DT, false>(g, (int)pc, lane, 32);
+                        }
                     }
                 }
                 __syncthreads();
+                // pieces of 257..BIG_CHUNK keys: shared-memory bitonic by all
+                // threads, one at a time
+                const uint32_t nwb = min(S.nwbig, (uint32_t)BIG_MAXWBIG);
+                for (uint32_t k = 0; k < nwb; k++) {
+                    const uint32_t d = S.wbig[k];
+                    bitonic<DT, true>(sk + (S.start[d] - slo), (int)(S.end[d] - S.start[d]), tid, bd);
+                }
                 BG_PROF(8);
                 for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
                 __syncthreads();

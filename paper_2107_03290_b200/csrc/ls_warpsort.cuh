@@ -197,8 +197,9 @@ __device__ __forceinline__ void warp_sort_keys(uint64_t *g, uint32_t pc, int lan
 
 // Same for a piece whose ords all lie in [base, base + 2^32): peeling works on
 // 32-bit offsets with single-instruction warp reductions (REDUX), so a piece
-// with up to PEEL distinct values costs PEEL short rounds.
-template <int DT, int NS, int PEEL = 16>
+// with up to PEEL distinct values costs PEEL short rounds (4: measured on
+// config 4 against 2, 8 and 16 -- each round also writes its run).
+template <int DT, int NS, int PEEL = 4>
 __device__ __forceinline__ void warp_sort_keys_rel(uint64_t *g, uint32_t pc, unsigned long long base,
                                                    int lane) {
     uint32_t v[NS];
