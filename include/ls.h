@@ -47,6 +47,12 @@ typedef enum {
 /* flags */
 #define LS_FLAG_PHASE_TIMING 0x1ULL /* record CUDA events between phases (ls_stats.phase_ms) */
 #define LS_FLAG_VALIDATE_MODEL 0x2ULL /* ls_sort_with_model: reject unsafe models (default on) */
+#define LS_FLAG_FUSED_ROUND1 0x4ULL /* ls_sort: partition every level-0 bucket of 64K..~219K keys
+                                       with one 8-CTA cluster (count and scatter of
+                                       round 1 in one kernel, the bucket staged in shared memory,
+                                       the histogram exchanged through DSMEM). Same output, ids
+                                       and S'_B; off by default: measured slower on B200
+                                        */
 
 /* Algorithm constants (fan-out 1000, 1000 leaves, 1% sample) and the
  * free tuning knob big_threshold (R-Q22: sub-buckets above it take the exact
@@ -94,6 +100,7 @@ typedef struct {
     uint64_t max_group;                 /* largest run of equal counting-sort positions       */
     uint64_t big_passes;                /* radix passes spent on big sub-buckets              */
     uint64_t kernel_launches;           /* kernels this call launched                         */
+    uint64_t fused_buckets;             /* level-0 buckets partitioned cluster-resident (f2)  */
     float phase_ms[LS_NUM_PHASES];      /* with LS_FLAG_PHASE_TIMING                          */
 } ls_stats;
 

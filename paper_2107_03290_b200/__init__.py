@@ -11,7 +11,8 @@ import ctypes as C
 
 from . import _lib
 from ._lib import (LS_E_CAPACITY, LS_E_CUDA, LS_E_INTERNAL, LS_E_INVALID, LS_E_NAN, LS_E_NCCL,
-                   LS_E_WORKSPACE, LS_F64, LS_FLAG_PHASE_TIMING, LS_OK, LS_U64, PHASES, Config,
+                   LS_E_WORKSPACE, LS_F64, LS_FLAG_FUSED_ROUND1, LS_FLAG_PHASE_TIMING, LS_OK,
+                   LS_U64, PHASES, Config,
                    Dumps, Leaf, Model, Stats, Tagged)
 
 lib = _lib.load()
@@ -22,7 +23,7 @@ __all__ = [
     "multi_workspace_bytes", "multi_splitters", "multi_plan", "multi_dest", "Config", "Model",
     "Stats", "Dumps", "Tagged", "Leaf", "PHASES", "LS_F64", "LS_U64", "LS_OK", "LS_E_NAN",
     "LS_E_INVALID", "LS_E_WORKSPACE", "LS_E_CAPACITY", "LS_E_CUDA", "LS_E_NCCL", "LS_E_INTERNAL",
-    "LS_FLAG_PHASE_TIMING",
+    "LS_FLAG_PHASE_TIMING", "LS_FLAG_FUSED_ROUND1",
 ]
 
 

@@ -13,6 +13,7 @@ LS_MAX_FANOUT = 1024
 LS_MAX_LEAVES = 1024
 LS_FLAG_PHASE_TIMING = 0x1
 LS_FLAG_VALIDATE_MODEL = 0x2
+LS_FLAG_FUSED_ROUND1 = 0x4
 LS_UNIQUE_ID_BYTES = 128
 PHASES = ("fit", "count0", "scatter0", "count1", "scatter1", "classify", "bucketsort", "big")
 
@@ -47,7 +48,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "n", "h0_buckets", "h0_keys", "h1_subbuckets", "h1_keys", "small_subbuckets",
         "small_keys", "big_subbuckets", "big_keys", "max_group", "big_passes",
-        "kernel_launches")] + [("phase_ms", C.c_float * len(PHASES))]
+        "kernel_launches", "fused_buckets")] + [("phase_ms", C.c_float * len(PHASES))]
 
     def as_dict(self) -> dict:
         d = {n: int(getattr(self, n)) for n, _ in self._fields_[:-1]}

@@ -41,7 +41,7 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
@@ -105,6 +105,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.ctasks = take((size_t)l.task_cap * 16);
     l.ctasks2 = take((size_t)l.task_cap * 16);
     l.ctasks3 = take((size_t)l.task_cap * 16);
+    l.fused = take((size_t)l.f * 4);
+    l.flist = take((size_t)l.f * 4);
     l.large = take((size_t)l.lcap * 4);
     l.lstart = take((size_t)l.lcap * 1024 * 4);
     l.lcur = take((size_t)l.lcap * 1024 * 4);
@@ -166,6 +168,8 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.ctasks = (uint4 *)(w + l.ctasks);
     a.ctasks2 = (uint4 *)(w + l.ctasks2);
     a.ctasks3 = (uint4 *)(w + l.ctasks3);
+    a.fused = (uint32_t *)(w + l.fused);
+    a.flist = (uint32_t *)(w + l.flist);
     a.large = (uint32_t *)(w + l.large);
     a.lcap = l.lcap;
     a.pcap = l.pcap;
@@ -298,6 +302,11 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
     Args a = make_args(l, d_keys, d_ws);
     if (const char *e = getenv("LS_DEBUG_STAGE")) a.dbg = (uint32_t)atoi(e);
+    // cluster-resident round 1 with LS_FLAG_FUSED_ROUND1; LS_FR_MIN
+    // overrides the smallest bucket it takes (tests)
+    a.fr_cap = (cfg.flags & LS_FLAG_FUSED_ROUND1) ? round1_capacity() : 0u;
+    a.fr_min = a.fr_cap ? FR_MIN_DEFAULT : 0u;
+    if (const char *e = getenv("LS_FR_MIN")) a.fr_min = a.fr_cap ? (uint32_t)atoi(e) : 0u;
     const int dt = (int)dtype;
     unsigned char *w = (unsigned char *)d_ws;
     if (dumps) {
@@ -335,6 +344,10 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     launch_scatter0(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_SCATTER0);
+    if (a.fr_min) {  // buckets that fit a CTA cluster: count + scatter of round 1 in one kernel
+        launch_round1(a, dt, st);
+        launches++;
+    }
     launch_count1(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_COUNT1);
@@ -396,6 +409,7 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
         stats->max_group = c.stat[ST_MAXGRP];
         stats->big_passes = c.stat[ST_BIGPASS];
         stats->kernel_launches = pend->launches;
+        stats->fused_buckets = c.nfused;
     }
     if (pend->timer_on) {
         if (stats)

@@ -228,6 +228,7 @@ __host__ __device__ __forceinline__ int size_class(uint32_t np, uint32_t T_small
     if (np <= CM_MAX) return SC_CTAM;
     return SC_CTA;
 }
+constexpr uint32_t FR_MIN_DEFAULT = 65536;  // smallest level-0 bucket for the cluster-resident round 1
 constexpr uint32_t LARGE_MIN = 262144;  // big sub-buckets above this: grid-parallel path (ls_bigpath.cu)
 
 struct Ctl {
@@ -241,6 +242,7 @@ struct Ctl {
     uint32_t nctask, nctask2, nctask3; // CTA sub-bucket sorts: SC_CTA, SC_CTAM, SC_CTAL (k_classify)
     uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
     uint32_t nfill;                    // homogeneous pieces of large items (k_large_fill)
+    uint32_t nfused, fticket;          // cluster-resident round 1: buckets listed / taken
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
     unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
@@ -301,6 +303,11 @@ struct Args {
     unsigned long long *lmin, *lmax;  // [lcap*1024]
     uint2 *pieces;                    // [pcap] small non-homogeneous pieces {off, size} (in B)
     uint4 *fills;                     // [fcap] homogeneous pieces {off, size, ord lo, ord hi}
+    // cluster-resident round 1 (ls_round1.cu): level-0 buckets of fr_min..fr_cap
+    // keys (fr_min = 0: off) are partitioned by one CTA cluster each
+    uint32_t *fused;                  // [f] 1: bucket taken by k_round1 (k_count1/k_scatter1 skip it)
+    uint32_t *flist;                  // [f] the taken buckets
+    uint32_t fr_min, fr_cap;
     uint32_t fcap;
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]

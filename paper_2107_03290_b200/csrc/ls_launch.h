@@ -26,6 +26,10 @@ void launch_count1(const Args &a, int dtype, cudaStream_t st);
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st);
 void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st);
 
+// cluster-resident round 1 (ls_round1.cu)
+uint32_t round1_capacity();  // keys per cluster (0: clusters unavailable)
+void launch_round1(const Args &a, int dtype, cudaStream_t st);
+
 // in-bucket sort (ls_sortsub.cu)
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);

@@ -29,6 +29,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = 0;
+        ctl->nfused = ctl->fticket = 0;
         ctl->nlarge = ctl->npiece = 0;
         ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
@@ -157,6 +158,11 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     for (int b = tid; b < f; b += blockDim.x) {
         a.start0[b] = s[b];
         a.unit1_start[b] = nu[b];
+        // cluster-resident round 1 (ls_round1.cu) for buckets of fr_min..fr_cap keys
+        const uint64_t h = a.hist0[b];
+        const bool fu = a.fr_min != 0 && h >= a.fr_min && h <= a.fr_cap;
+        a.fused[b] = fu ? 1u : 0u;
+        if (fu) a.flist[atomicAdd(&a.ctl->nfused, 1u)] = (uint32_t)b;
     }
     if (tid == 0) {
         a.start0[f] = total;
@@ -229,6 +235,7 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     const uint32_t u = s_unit;
     if (u >= a.ctl->U1 || a.ctl->status) return;
     const int b = find_bucket(ustart, f, u);
+    if (a.fused[b]) return;  // partitioned by k_round1
     const uint32_t slice = u - ustart[b];
     const uint64_t bend = a.start0[b + 1];
     const uint64_t beg = a.start0[b] + (uint64_t)slice * a.C1;
@@ -311,6 +318,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     for (int b = tid; b <= f; b += bd) S.ustart[b] = a.unit1_start[b];
     __syncthreads();
     const int b = find_bucket(S.ustart, f, u);
+    if (a.fused[b]) return;  // partitioned by k_round1
     const uint32_t slice = u - S.ustart[b];
     const uint64_t bbeg = a.start0[b], bend = a.start0[b + 1];
     const uint64_t beg = bbeg + (uint64_t)slice * a.C1;

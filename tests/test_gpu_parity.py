@@ -144,6 +144,33 @@ def test_sort_bit_exact_1e7(dist):
     check_sort(gen(dist, 10_000_000, 11))
 
 
+# ------------------------------------------ cluster-resident round 1 (f2) --
+
+FUSED = dict(flags=ls.LS_FLAG_FUSED_ROUND1)
+
+
+@pytest.mark.parametrize("dist", ["normal", "uniform01", "mixgauss", "zipf", "rootdups", "twodups",
+                                  "telemetry"])
+def test_fused_round1_bit_exact(dist, monkeypatch):
+    """SURVEY §8(f) f2 (LS_FLAG_FUSED_ROUND1): level-0 buckets partitioned by
+    one 8-CTA cluster each (forced down to small buckets with LS_FR_MIN;
+    Zipf's and config 4's largest buckets exceed the cluster and take the
+    separate path in the same call) give the oracle's output, S_B, S'_B, H0
+    and H1, as the default separate count/scatter path does."""
+    monkeypatch.setenv("LS_FR_MIN", "256")
+    keys = gen(dist, 3_000_000, 13)
+    st, _ = check_sort(keys, cfg=ls.config(**FUSED))
+    assert st["fused_buckets"] > 0
+    st2, _ = check_sort(keys)
+    assert st2["fused_buckets"] == 0
+
+
+def test_fused_round1_default_threshold():
+    """At 70M keys the level-0 buckets (~70K keys) take the cluster path."""
+    st, _ = check_sort(gen("normal", 70_000_000, 17), cfg=ls.config(**FUSED))
+    assert st["fused_buckets"] >= 990
+
+
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 31, 99, 100, 101, 2047, 2048, 2049, 4097, 8191, 8192,
                                8193, 65535, 65536, 65537, 131073, 300_001])
 def test_sort_sizes(n):
