@@ -432,9 +432,16 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         if (sc == SC_TRIVIAL) {
             if (a.dH1) a.dH1[g] = 1;
         } else if (sc == SC_WINDOW) {  // tiny sub-buckets: block windows
+            // (the first / last window sub-bucket of each tile among this
+            // warp's lanes does the atomics: st and g grow with the lane)
             const uint32_t t = st / a.T_tile;
-            atomicMin(&a.tile_first[t], (uint32_t)g);
-            atomicMax(&a.tile_last[t], (uint32_t)g);
+            const uint32_t wm = __activemask();
+            const int lane = tid & 31;
+            const uint32_t below = wm & ((1u << lane) - 1u), above = wm & ~((2u << lane) - 1u);
+            const uint32_t tp = __shfl_sync(wm, t, below ? 31 - __clz(below) : lane);
+            const uint32_t tn = __shfl_sync(wm, t, above ? __ffs(above) - 1 : lane);
+            if (!below || tp != t) atomicMin(&a.tile_first[t], (uint32_t)g);
+            if (!above || tn != t) atomicMax(&a.tile_last[t], (uint32_t)g);
         } else if (sc == SC_BIG) {
             const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
             if (k < a.big_cap) {

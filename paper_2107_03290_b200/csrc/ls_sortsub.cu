@@ -611,6 +611,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     if (threadIdx.x < 4) st_red[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t ntask = min(a.ctl->ntask, a.task_cap);
+    if (blockIdx.x * WS_WARPS >= ntask) return;  // (no task for this block: skip the model reads)
     const Root R = load_root(a.M);
     const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
@@ -863,6 +864,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PadT T{S.T, 0u};
     const uint32_t ntask = min(*count, a.task_cap);
+    if (blockIdx.x >= ntask) return;  // (no task for this block: skip the model reads)
     const Root R = load_root(a.M);
     const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
