@@ -198,11 +198,17 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Scatter0Smem &S = *reinterpret_cast<Scatter0Smem *>(smem_raw);
     const int f = a.f, tid = threadIdx.x;
-    const uint64_t u = blockIdx.x;
+    // a contiguous run of count0 units [u0, u1) per CTA: the cursors of unit
+    // u0 (count0's lookback offsets) run on into u0 + 1, ... because those
+    // offsets are exclusive prefix sums over the units (one tile stream, one
+    // search-table load and one pipeline start per CTA instead of per unit)
+    const uint64_t u0 = (uint64_t)blockIdx.x * a.U0 / gridDim.x;
+    const uint64_t u1 = (uint64_t)(blockIdx.x + 1) * a.U0 / gridDim.x;
+    if (u1 <= u0) return;
     const B0Bucket<DT> bf{load_b0_search(S.b0, a.M)};
-    if (tid < f) S.base[tid] = (uint32_t)a.start0[tid] + a.offs0[u * f + tid];
+    if (tid < f) S.base[tid] = (uint32_t)a.start0[tid] + a.offs0[u0 * f + tid];
     tp_init(S.tp);
-    const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
+    const uint64_t beg = u0 * a.C0, end = umin64(a.n, u1 * a.C0);
     uint32_t phase = 0;
     tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase, nullptr, nullptr,
                    (a.dbg & 1024u) ? a.ctl->prof : nullptr);
@@ -516,8 +522,12 @@ void launch_count0(const Args &a, int dtype, cudaStream_t st) {
 void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st) { k_plan0<<<1, 1024, 0, st>>>(a, dS_B); }
 void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(Scatter0Smem);
-    if (dtype == DT_F64) { set_smem(k_scatter0<DT_F64>, sm); k_scatter0<DT_F64><<<a.U0, TP_THREADS, sm, st>>>(a); }
-    else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<a.U0, TP_THREADS, sm, st>>>(a); }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = a.U0 < (uint32_t)sms ? a.U0 : (unsigned)sms;  // one CTA per SM (smem-bound)
+    if (dtype == DT_F64) { set_smem(k_scatter0<DT_F64>, sm); k_scatter0<DT_F64><<<g, TP_THREADS, sm, st>>>(a); }
+    else { set_smem(k_scatter0<DT_U64>, sm); k_scatter0<DT_U64><<<g, TP_THREADS, sm, st>>>(a); }
 }
 void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = (size_t)5 * a.L * sizeof(double);
