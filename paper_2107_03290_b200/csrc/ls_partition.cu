@@ -139,6 +139,18 @@ __global__ void __launch_bounds__(512, 2) k_count0(Args a) {
     }
 }
 
+// Round-1 units: a bucket of h keys is cut into nu = max(1, round(h / C1))
+// units of ceil(h / nu) keys rounded up to whole scatter tiles (not C1-sized
+// units plus a sliver, which would cost a whole CTA start and a partial tile).
+__host__ __device__ __forceinline__ uint32_t unit1_count(uint64_t h, uint32_t C1) {
+    const uint64_t nu = (h + C1 / 2) / C1;
+    return h == 0 ? 0u : (uint32_t)(nu ? nu : 1);
+}
+__device__ __forceinline__ uint64_t unit1_size(uint64_t bbeg, uint64_t bend, uint32_t nu) {
+    const uint64_t u = nu ? (bend - bbeg + nu - 1) / nu : 1;
+    return (u + TP_TILE - 1) / TP_TILE * TP_TILE;
+}
+
 // S_B (Alg. 1 output), bucket starts (Alg. 2 read head) and the
 // round-1 unit plan. One block.
 __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
@@ -149,7 +161,7 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     for (int b = tid; b < f; b += blockDim.x) {
         const uint64_t h = a.hist0[b];
         s[b] = (uint32_t)h;
-        nu[b] = (uint32_t)((h + a.C1 - 1) / a.C1);
+        nu[b] = unit1_count(h, a.C1);
         if (dS_B) dS_B[b] = h;
     }
     __syncthreads();
@@ -244,8 +256,9 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     if (a.fused[b]) return;  // partitioned by k_round1
     const uint32_t slice = u - ustart[b];
     const uint64_t bend = a.start0[b + 1];
-    const uint64_t beg = a.start0[b] + (uint64_t)slice * a.C1;
-    const uint64_t end = umin64(bend, beg + a.C1);
+    const uint64_t usz = unit1_size(a.start0[b], bend, ustart[b + 1] - ustart[b]);
+    const uint64_t beg = umin64(bend, a.start0[b] + (uint64_t)slice * usz);  // (tile rounding can
+    const uint64_t end = umin64(bend, beg + usz);                           //  leave a unit empty)
     const Root R = load_root(a.M);
     unsigned long long mn = ~0ull, mx = 0;
     auto one = [&](uint64_t key) -> uint32_t {
@@ -327,8 +340,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     if (a.fused[b]) return;  // partitioned by k_round1
     const uint32_t slice = u - S.ustart[b];
     const uint64_t bbeg = a.start0[b], bend = a.start0[b + 1];
-    const uint64_t beg = bbeg + (uint64_t)slice * a.C1;
-    const uint64_t end = umin64(bend, beg + a.C1);
+    const uint64_t usz = unit1_size(bbeg, bend, S.ustart[b + 1] - S.ustart[b]);
+    const uint64_t beg = umin64(bend, bbeg + (uint64_t)slice * usz);  // (may be empty: tile rounding)
+    const uint64_t end = umin64(bend, beg + usz);
     const unsigned long long mn = a.bmin0[b];
     if (bend - bbeg <= 1 || mn == a.bmax0[b]) {
         // homogeneous level-0 bucket: already in final position
