@@ -144,8 +144,9 @@ __device__ __forceinline__ void warp_sort_piece(uint64_t *g, uint32_t pc, int la
 // Sort pc <= 32*NS keys of g (shared or global memory, key bits; DT order) by
 // one warp. Pieces with few distinct values (duplicate-heavy inputs) are
 // emitted by peeling: up to PEEL rounds of (warp minimum of the remaining
-// keys, how many equal it, write that run); only if more distinct values
-// remain is the full register bitonic network run.
+// keys, how many equal it, write that run); once more distinct values remain,
+// or a peeled minimum had at most 2 copies (a piece of mostly distinct keys),
+// the rest goes through the register bitonic network.
 template <int DT, int NS, int PEEL = 4>
 __device__ __forceinline__ void warp_sort_keys(uint64_t *g, uint32_t pc, int lane) {
     uint64_t v[NS];
@@ -179,6 +180,7 @@ __device__ __forceinline__ void warp_sort_keys(uint64_t *g, uint32_t pc, int lan
         for (uint32_t i = out + lane; i < out + tot; i += 32) g[i] = key;
         out += tot;
         if (out >= pc) return;
+        if (tot <= 2) break;  // a (nearly) unique minimum: few duplicates, the network is cheaper
     }
     __syncwarp();
     // more than PEEL distinct values: sort the remaining keys (the peeled ones
@@ -229,6 +231,7 @@ __device__ __forceinline__ void warp_sort_keys_rel(uint64_t *g, uint32_t pc, uns
         for (uint32_t i = out + lane; i < out + tot; i += 32) g[i] = key;
         out += tot;
         if (out >= pc) return;
+        if (tot <= 2) break;  // a (nearly) unique minimum: few duplicates, the network is cheaper
     }
     __syncwarp();
     // more than PEEL distinct values: bitonic on the remaining offsets (the
