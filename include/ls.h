@@ -119,7 +119,7 @@ const char *ls_status_string(ls_status s);
 const char *ls_last_error(void);
 
 /* Device workspace needed by ls_sort / ls_sort_with_model / ls_train_rmi /
- * ls_bucket_ids for n keys (CUB-style size query). About 12n bytes + ~60 MB:
+ * ls_bucket_ids for n keys (CUB-style size query). About 12n bytes + ~90 MB:
  * the scratch copy B of Alg. 2's partition rounds (8n), the round-1 bucket
  * ids (2n), the in-bucket task lists and big-item lists, per-unit tables. */
 ls_status ls_workspace_bytes(uint64_t n, ls_dtype dtype, const ls_config *cfg, size_t *bytes);
@@ -136,7 +136,10 @@ ls_status ls_train_rmi(const void *d_sample, uint64_t m, ls_dtype dtype, const l
 /* Sort n keys in place (Alg. 2): strided sample + fit, level-0
  * partition (count -> decoupled-lookback offsets -> scatter), level-1
  * segmented partition, homogeneous-bucket skip, model counting sort with
- * collision-group touch-up, exact big-bucket path. dumps/stats may be NULL. */
+ * collision-group touch-up, exact big-bucket path. dumps/stats may be NULL.
+ * d_keys must be 16-byte aligned and d_ws 256-byte aligned (cudaMalloc /
+ * torch allocations are; an odd-offset slice is not): LS_E_INVALID otherwise,
+ * for every entry point that takes device keys and a workspace. */
 ls_status ls_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg, void *d_ws,
                   size_t ws_bytes, void *stream, ls_stats *stats, const ls_dumps *dumps);
 
@@ -204,6 +207,26 @@ ls_status ls_multi_plan(const uint64_t *h_counts, int world, int rank, uint64_t 
  * (ord(x), rank, index) in lexicographic order. Host reference of the device rule. */
 int ls_multi_dest(const ls_tagged *h_splitters, int world, uint64_t ord, uint32_t rank,
                   uint64_t index);
+
+/* The device steps of ls_sort_multi for ONE rank, without a communicator, so
+ * the routing kernels run for world > 1 on a single GPU (tests): nothing
+ * waits on another rank.
+ * ls_multi_sample: step 1, the LS_MULTI_SAMPLE tagged split-sample entries of
+ *   this rank's shard d_in[n_in] into d_samples (device, caller-owned; entries
+ *   beyond n_in are sentinels with rank 0xffffffff).
+ * ls_multi_route: steps 3 + 5 with the given R-1 splitters (host): the
+ *   destination counts (h_counts[world], host) and the shard regrouped by
+ *   destination into d_send[n_in] (device; destination p's keys start at
+ *   sum_{q<p} h_counts[q], in no particular order inside). d_ws holds at least
+ *   ls_multi_workspace_bytes(n_in, 0, world, ...) bytes. Synchronous on
+ *   `stream`. Errors: LS_E_INVALID (bad sizes / world), LS_E_WORKSPACE,
+ *   LS_E_NAN (NaN key; d_send untouched). */
+#define LS_MULTI_SAMPLE 4096
+ls_status ls_multi_sample(const void *d_in, uint64_t n_in, int rank, ls_dtype dtype,
+                          ls_tagged *d_samples, void *stream);
+ls_status ls_multi_route(const void *d_in, uint64_t n_in, int rank, int world,
+                         const ls_tagged *h_splitters, ls_dtype dtype, void *d_send,
+                         uint64_t *h_counts, void *d_ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,8 @@ lib = _lib.load()
 __all__ = [
     "lib", "LSError", "config", "dtype_code", "workspace_bytes", "workspace", "ls_train_rmi",
     "ls_sort", "ls_sort_with_model", "ls_sort_host", "ls_bucket_ids", "Comm", "ls_sort_multi",
-    "multi_workspace_bytes", "multi_splitters", "multi_plan", "multi_dest", "Config", "Model",
+    "multi_workspace_bytes", "multi_splitters", "multi_plan", "multi_dest", "multi_sample",
+    "multi_route", "Config", "Model",
     "Stats", "Dumps", "Tagged", "Leaf", "PHASES", "LS_F64", "LS_U64", "LS_OK", "LS_E_NAN",
     "LS_E_INVALID", "LS_E_WORKSPACE", "LS_E_CAPACITY", "LS_E_CUDA", "LS_E_NCCL", "LS_E_INTERNAL",
     "LS_FLAG_PHASE_TIMING", "LS_FLAG_FUSED_ROUND1",
@@ -228,6 +229,38 @@ def multi_plan(counts, world: int, rank: int):
     _check(lib.ls_multi_plan(counts.ctypes.data, world, rank, sd.ctypes.data, rc_.ctypes.data,
                              rd.ctypes.data, C.byref(n_out)), "ls_multi_plan")
     return sd, rc_, rd, n_out.value
+
+
+TAGGED_DTYPE = [("ord", "<u8"), ("rank", "<u4"), ("pad", "<u4"), ("index", "<u8")]
+
+
+def multi_sample(keys, rank: int, stream=None):
+    """The LS_MULTI_SAMPLE tagged split-sample entries of one rank's shard
+    (step 1 of ls_sort_multi), as a numpy structured array."""
+    import numpy as np
+    import torch
+    d = torch.empty(_lib.LS_MULTI_SAMPLE * 24, dtype=torch.uint8, device=keys.device)
+    _check(lib.ls_multi_sample(_ptr(keys), keys.numel(), rank, dtype_code(keys), _ptr(d),
+                               _stream(stream)), "ls_multi_sample")
+    return d.cpu().numpy().view(np.dtype(TAGGED_DTYPE)).copy()
+
+
+def multi_route(keys, rank: int, world: int, splitters, send, ws=None, stream=None):
+    """Steps 3 + 5 of ls_sort_multi for one rank without a communicator: returns
+    the destination counts; send[:n] holds the shard grouped by destination."""
+    import numpy as np
+    import torch
+    dt = dtype_code(keys)
+    if ws is None:
+        ws = torch.empty(multi_workspace_bytes(keys.numel(), 0, world, dt), dtype=torch.uint8,
+                         device=keys.device)
+    spl = np.ascontiguousarray(splitters)
+    counts = np.zeros(world, np.uint64)
+    _check(lib.ls_multi_route(_ptr(keys), keys.numel(), rank, world,
+                              spl.ctypes.data if len(spl) else None, dt, _ptr(send),
+                              counts.ctypes.data, _ptr(ws), ws.numel(), _stream(stream)),
+           "ls_multi_route")
+    return counts
 
 
 def multi_dest(splitters, world: int, ord_: int, rank: int, index: int) -> int:

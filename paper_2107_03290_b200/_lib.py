@@ -14,6 +14,7 @@ LS_MAX_LEAVES = 1024
 LS_FLAG_PHASE_TIMING = 0x1
 LS_FLAG_VALIDATE_MODEL = 0x2
 LS_FLAG_FUSED_ROUND1 = 0x4
+LS_MULTI_SAMPLE = 4096
 LS_UNIQUE_ID_BYTES = 128
 PHASES = ("fit", "count0", "scatter0", "count1", "scatter1", "classify", "bucketsort", "big")
 
@@ -22,7 +23,8 @@ EXPORTS = (
     "ls_config_default", "ls_status_string", "ls_last_error", "ls_workspace_bytes",
     "ls_train_rmi", "ls_sort", "ls_sort_with_model", "ls_sort_host", "ls_bucket_ids",
     "ls_comm_unique_id", "ls_comm_init", "ls_comm_destroy", "ls_multi_workspace_bytes",
-    "ls_sort_multi", "ls_multi_splitters", "ls_multi_plan", "ls_multi_dest",
+    "ls_sort_multi", "ls_multi_splitters", "ls_multi_plan", "ls_multi_dest", "ls_multi_sample",
+    "ls_multi_route",
 )
 
 
@@ -95,6 +97,8 @@ def load() -> C.CDLL:
         "ls_multi_splitters": (S, [P, U64, I, P]),
         "ls_multi_plan": (S, [P, I, I, P, P, P, C.POINTER(U64)]),
         "ls_multi_dest": (I, [P, I, U64, U32, U64]),
+        "ls_multi_sample": (S, [P, U64, I, I, P, P]),
+        "ls_multi_route": (S, [P, U64, I, I, P, I, P, P, P, C.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

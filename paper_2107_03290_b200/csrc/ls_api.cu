@@ -297,6 +297,11 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     if (stats) stats->n = n;
     if (n <= 1) return LS_OK;
     if (!d_keys || !d_ws) { set_error("null pointer"); return LS_E_INVALID; }
+    // the bulk-copy (TMA) stages and 16-byte vector loads address keys in aligned pairs
+    if (((uintptr_t)d_keys & 15) || ((uintptr_t)d_ws & 255)) {
+        set_error("keys must be 16-byte aligned and the workspace 256-byte aligned");
+        return LS_E_INVALID;
+    }
     if (inject && !model_ok(*inject, cfg)) { set_error("injected model is not monotone-safe"); return LS_E_INVALID; }
     const Layout l = make_layout(n, cfg);
     if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }

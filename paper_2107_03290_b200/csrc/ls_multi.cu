@@ -30,7 +30,7 @@ struct ls_comm {
 
 namespace ls {
 
-constexpr int SPLIT_K = 4096;        // sample entries per rank
+constexpr int SPLIT_K = LS_MULTI_SAMPLE;  // sample entries per rank
 constexpr uint32_t MULTI_UNIT = 65536;
 constexpr int MAX_WORLD = 64;
 
@@ -310,6 +310,10 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     if (!comm || !n_out || !d_ws || (n_in && !d_in) || (out_cap && !d_out)) { set_error("null pointer"); return LS_E_INVALID; }
     if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
     if (n_in >= (1ull << 32) || out_cap >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    if (((uintptr_t)d_in & 15) || ((uintptr_t)d_out & 15) || ((uintptr_t)d_ws & 255)) {
+        set_error("keys / output must be 16-byte aligned and the workspace 256-byte aligned");
+        return LS_E_INVALID;
+    }
     const int R = comm->world, me = comm->rank;
     const MultiLayout l = multi_layout(n_in, out_cap, R, cfg);
     if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
@@ -400,6 +404,88 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     rc = enqueue_sort(out, nout, dtype, &cfg, nullptr, w + l.local, ws_bytes - l.local, st, stats, nullptr, &pend);
     if (rc != LS_OK) return rc;
     return finish_sort(&pend, st, stats);
+}
+
+ls_status ls_multi_sample(const void *d_in, uint64_t n_in, int rank, ls_dtype dtype,
+                          ls_tagged *d_samples, void *stream) {
+    if (!d_samples || (n_in && !d_in) || rank < 0 || rank >= MAX_WORLD) { set_error("bad arguments"); return LS_E_INVALID; }
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == LS_F64) k_split_sample<DT_F64><<<(SPLIT_K + 255) / 256, 256, 0, st>>>((const uint64_t *)d_in, n_in, (uint32_t)rank, (Tagged *)d_samples);
+    else k_split_sample<DT_U64><<<(SPLIT_K + 255) / 256, 256, 0, st>>>((const uint64_t *)d_in, n_in, (uint32_t)rank, (Tagged *)d_samples);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    return LS_OK;
+}
+
+ls_status ls_multi_route(const void *d_in, uint64_t n_in, int rank, int world,
+                         const ls_tagged *h_splitters, ls_dtype dtype, void *d_send,
+                         uint64_t *h_counts, void *d_ws, size_t ws_bytes, void *stream) {
+    if (world < 1 || world > MAX_WORLD || rank < 0 || rank >= world || !h_counts || !d_ws ||
+        (world > 1 && !h_splitters) || (n_in && (!d_in || !d_send))) {
+        set_error("bad arguments");
+        return LS_E_INVALID;
+    }
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    if (n_in >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    if (((uintptr_t)d_in & 15) || ((uintptr_t)d_send & 15) || ((uintptr_t)d_ws & 255)) {
+        set_error("keys / send buffer must be 16-byte aligned and the workspace 256-byte aligned");
+        return LS_E_INVALID;
+    }
+    ls_config cfg;
+    ls_config_default(&cfg);
+    const int R = world;
+    const MultiLayout l = multi_layout(n_in, 0, R, cfg);
+    if (ws_bytes < l.local) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned char *w = (unsigned char *)d_ws;
+    const int dt = (int)dtype;
+    if (R > 1) CUDA_CHECK(cudaMemcpyAsync(w + l.spl, h_splitters, (size_t)(R - 1) * sizeof(Tagged), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemsetAsync(w + l.ticket, 0, l.send - l.ticket, st));
+    MultiArgs a;
+    a.in = (const uint64_t *)d_in;
+    a.send = (uint64_t *)d_send;
+    a.n = n_in;
+    a.rank = (uint32_t)rank;
+    a.world = R;
+    a.U = l.U;
+    a.spl = (const Tagged *)(w + l.spl);
+    a.lb = (unsigned long long *)(w + l.lb);
+    a.offs = (uint32_t *)(w + l.offs);
+    a.counts = (unsigned long long *)(w + l.counts);
+    a.sdispl = (const unsigned long long *)(w + l.sdispl);
+    a.ticket = (uint32_t *)(w + l.ticket);
+    // step 3 of ls_sort_multi: destination counts, per-unit offsets
+    if (n_in) {
+        if (dt == DT_F64) k_dest_count<DT_F64><<<l.U, 512, 0, st>>>(a);
+        else k_dest_count<DT_U64><<<l.U, 512, 0, st>>>(a);
+    }
+    std::vector<unsigned long long> row((size_t)R + 1);
+    CUDA_CHECK(cudaMemcpyAsync(row.data(), a.counts, row.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (row[R]) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
+    std::vector<uint64_t> sd(R);
+    uint64_t s = 0;
+    for (int p = 0; p < R; p++) {
+        h_counts[p] = row[p];
+        sd[p] = s;
+        s += row[p];
+    }
+    // step 5: scatter by destination
+    CUDA_CHECK(cudaMemcpyAsync(w + l.sdispl, sd.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
+    if (n_in) {
+        const size_t sm = sizeof(DestSmem);
+        if (dt == DT_F64) {
+            cudaFuncSetAttribute(k_dest_scatter<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_dest_scatter<DT_F64><<<l.U, TP_THREADS, sm, st>>>(a);
+        } else {
+            cudaFuncSetAttribute(k_dest_scatter<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_dest_scatter<DT_U64><<<l.U, TP_THREADS, sm, st>>>(a);
+        }
+    }
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    return LS_OK;
 }
 
 }  // extern "C"

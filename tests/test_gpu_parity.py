@@ -213,6 +213,18 @@ def test_sort_edge_cases(name):
         assert np.array_equal(bits(to_np(t)), bits(O.sort(h, cfg=ocfg)[0]))
 
 
+def test_misaligned_keys_rejected():
+    """Keys at an odd 8-byte offset (a tensor slice) are rejected before any
+    work, as include/ls.h states: the TMA stages address aligned key pairs."""
+    keys = gen("normal", 10_001, 5)
+    view = keys[1:]
+    before = to_np(view).copy()
+    with pytest.raises(ls.LSError) as e:
+        ls.ls_sort(view)
+    assert e.value.status == ls.LS_E_INVALID
+    assert np.array_equal(bits(to_np(view)), bits(before))
+
+
 def test_nan_rejected_input_untouched():
     a = np.random.default_rng(1).standard_normal(100_000)
     a[54_321] = np.nan
@@ -355,6 +367,66 @@ def test_sort_multi_single_rank():
         assert e.value.status == ls.LS_E_CAPACITY
     finally:
         comm.close()
+
+
+def ord_np(a):
+    """IEEE totalOrder key (R12) of fp64 / identity for u64, as uint64."""
+    b = bits(a).astype(np.uint64)
+    if a.dtype == np.float64:
+        neg = (b >> np.uint64(63)) == 1
+        return np.where(neg, ~b, b | np.uint64(1 << 63))
+    return b
+
+
+@pytest.mark.parametrize("world,dist", [(2, "normal"), (3, "zipf"), (4, "twodups"),
+                                        (8, "cfg5mix"), (5, "telemetry")])
+def test_multi_route_world_gt1(world, dist):
+    """§8(e) for R > 1 ranks on one GPU, without a communicator (nothing waits
+    on another rank): each virtual rank's split sample (ls_multi_sample), the
+    splitters of the gathered samples, and each rank's destination counts and
+    send buffer (ls_multi_route: k_dest_count + k_dest_scatter, steps 3 and 5
+    of ls_sort_multi). Checked: every key's destination equals the
+    lexicographic (ord, rank, index) rule recomputed on the host, each
+    destination receives exactly that multiset, and sorting the destinations
+    one by one (the local ls_sort of step 7) and concatenating them gives the
+    oracle's global order."""
+    rng = np.random.default_rng(world)
+    n = 1_500_007
+    keys = gen(dist, n, 31)
+    h = to_np(keys)
+    cuts = np.concatenate([[0], np.sort(rng.choice(np.arange(1, n), world - 1, replace=False)), [n]])
+    shards = [keys[cuts[r]:cuts[r + 1]].clone() for r in range(world)]  # (aligned copies)
+    gathered = np.concatenate([ls.multi_sample(sh, r) for r, sh in enumerate(shards)])
+    spl = ls.multi_splitters(gathered.copy(), world)
+    recv = [[] for _ in range(world)]
+    for r, sh in enumerate(shards):
+        send = torch.empty_like(sh)
+        counts = ls.multi_route(sh, r, world, spl, send)
+        assert int(counts.sum()) == sh.numel()
+        # host rule: dest = #splitters below (ord, r, i)
+        o = ord_np(to_np(sh))
+        idx = np.arange(sh.numel(), dtype=np.uint64)
+        dest = np.zeros(sh.numel(), np.int64)
+        for s_ in spl:
+            so, sr, si = np.uint64(s_["ord"]), np.uint32(s_["rank"]), np.uint64(s_["index"])
+            below = (so < o) | ((so == o) & ((sr < np.uint32(r)) | ((sr == np.uint32(r)) & (si < idx))))
+            dest += below
+        assert np.array_equal(np.bincount(dest, minlength=world).astype(np.uint64), counts)
+        sent = to_np(send)
+        sd = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        for p in range(world):
+            part = sent[sd[p]:sd[p + 1]]
+            want = to_np(sh)[dest == p]
+            assert np.array_equal(np.sort(ord_np(part)), np.sort(ord_np(want)))
+            recv[p].append(part)
+    out = []
+    for p in range(world):
+        rp = np.concatenate(recv[p]) if recv[p] else np.zeros(0, h.dtype)
+        t = from_np(rp)
+        if t.numel():
+            ls.ls_sort(t)
+        out.append(to_np(t))
+    assert np.array_equal(bits(np.concatenate(out)), bits(O.sort(h)[0]))
 
 
 # -------------------------------------------------- large big sub-buckets --
