@@ -43,9 +43,15 @@ def test_host_only_entry_points():
     assert ls.lib.ls_sort(None, 1, 0, None, None, 0, None, C.byref(st), None) == ls.LS_OK
     assert ls.lib.ls_sort(C.c_void_p(16), 1 << 32, 0, None, C.c_void_p(16), 1 << 40, None,
                           None, None) == ls.LS_E_INVALID
-    assert ls.lib.ls_sort(C.c_void_p(16), 100, 0, None, C.c_void_p(16), 1, None, None,
+    assert ls.lib.ls_sort(C.c_void_p(16), 100, 0, None, C.c_void_p(256), 1, None, None,
                           None) == ls.LS_E_WORKSPACE
     assert b"workspace" in ls.lib.ls_last_error()
+    # keys at an odd 8-byte offset / an unaligned workspace: rejected before any work
+    assert ls.lib.ls_sort(C.c_void_p(24), 100, 0, None, C.c_void_p(256), 1 << 40, None, None,
+                          None) == ls.LS_E_INVALID
+    assert b"aligned" in ls.lib.ls_last_error()
+    assert ls.lib.ls_sort(C.c_void_p(16), 100, 0, None, C.c_void_p(272), 1 << 40, None, None,
+                          None) == ls.LS_E_INVALID
     # structure sizes agree with the header (offsets of the trailing members)
     assert C.sizeof(ls.Model) == 4 + 4 + 8 + 4 + 4 + 3 * 8 + 1024 * 40
     assert C.sizeof(ls.Tagged) == 24
