@@ -174,10 +174,18 @@ struct B0Search {
     const uint16_t *cell;
     template <int DT>
     __device__ __forceinline__ uint32_t get(uint64_t bits) const {
-        const uint32_t e = cell[b0_cell<DT>(bits, xmin, xmax, cs)];
+        const int c = b0_cell<DT>(bits, xmin, xmax, cs);
+        const uint32_t e = cell[c];
         uint32_t lo = e & 1023u, n = e >> 10;
-        if (n == 63u) n = nthr - lo;
+        if (n == 0u) return lo;  // most keys: no threshold inside their cell
         const unsigned long long o = to_ord<DT>(bits);
+        if (n == 1u) return lo + (thr[lo] <= o ? 1u : 0u);
+        if (n == 63u) {
+            // saturated count: the thresholds of cell c end where the next
+            // cell's begin (its offset, when that cell owns ords at all)
+            const uint32_t nx = c + 1 < B0_CELLS ? (cell[c + 1] & 1023u) : 0u;
+            n = (nx >= lo + 63u ? nx : nthr) - lo;
+        }
         while (n > 0) {
             const uint32_t half = n >> 1;
             if (thr[lo + half] <= o) {
