@@ -91,52 +91,57 @@ __global__ void __launch_bounds__(512, 2) k_count0(Args a) {
     __shared__ uint32_t s_unit;
     __shared__ int s_nan;
     const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
-    if (tid == 0) {
-        s_unit = atomicAdd(&a.ctl->ticket0, 1u);
-        s_nan = 0;
-    }
+    if (tid == 0) s_nan = 0;
+    // persistent: the b0 search tables are loaded once per CTA, then units
+    // (C0 keys each) are taken in ticket order (the lookback needs that order)
     const B0Search bs = load_b0_search(S.b0, a.M);
-    for (int b = tid; b < f; b += bd) hist[b] = 0;
-    __syncthreads();
-    const uint64_t u = s_unit;
-    const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
     bool nan = false;
     auto one = [&](uint64_t b) {
         if (DT == DT_F64 && is_nan_bits(b)) nan = true;
         atomicAdd(&hist[bs.get<DT>(b)], 1u);
     };
-    if ((((uintptr_t)(a.A + beg)) & 15) == 0) {
-        // 4 independent 16-byte loads in flight per thread
-        const ulonglong2 *A2 = (const ulonglong2 *)(a.A + beg);
-        const uint64_t np = (end - beg) / 2;
-        uint64_t i = tid;
-        for (; i + 3 * bd < np; i += 4 * bd) {
-            ulonglong2 v[4];
+    for (;;) {
+        if (tid == 0) s_unit = atomicAdd(&a.ctl->ticket0, 1u);
+        for (int b = tid; b < f; b += bd) hist[b] = 0;
+        __syncthreads();
+        const uint64_t u = s_unit;
+        if (u >= a.U0) break;
+        const uint64_t beg = u * a.C0, end = umin64(a.n, beg + a.C0);
+        if ((((uintptr_t)(a.A + beg)) & 15) == 0) {
+            // 4 independent 16-byte loads in flight per thread
+            const ulonglong2 *A2 = (const ulonglong2 *)(a.A + beg);
+            const uint64_t np = (end - beg) / 2;
+            uint64_t i = tid;
+            for (; i + 3 * bd < np; i += 4 * bd) {
+                ulonglong2 v[4];
 #pragma unroll
-            for (int q = 0; q < 4; q++) v[q] = __ldcs(A2 + i + q * bd);
+                for (int q = 0; q < 4; q++) v[q] = __ldcs(A2 + i + q * bd);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                one(v[q].x);
-                one(v[q].y);
+                for (int q = 0; q < 4; q++) {
+                    one(v[q].x);
+                    one(v[q].y);
+                }
             }
+            for (; i < np; i += bd) {
+                const ulonglong2 v = __ldcs(A2 + i);
+                one(v.x);
+                one(v.y);
+            }
+            if (((end - beg) & 1) && tid == 0) one(a.A[end - 1]);
+        } else {
+            for (uint64_t i = beg + tid; i < end; i += bd) one(a.A[i]);
         }
-        for (; i < np; i += bd) {
-            const ulonglong2 v = __ldcs(A2 + i);
-            one(v.x);
-            one(v.y);
+        __syncthreads();
+        for (int b = tid; b < f; b += bd) {
+            const uint32_t c = hist[b];
+            if (c) atomicAdd(&a.hist0[b], (unsigned long long)c);
+            a.offs0[u * f + b] = lookback(a.lb0, u, 0, f, b, c);
         }
-        if (((end - beg) & 1) && tid == 0) one(a.A[end - 1]);
-    } else {
-        for (uint64_t i = beg + tid; i < end; i += bd) one(a.A[i]);
+        __syncthreads();
     }
     if (nan) s_nan = 1;
     __syncthreads();
     if (tid == 0 && s_nan) atomicOr(&a.ctl->status, (uint32_t)STATUS_NAN);
-    for (int b = tid; b < f; b += bd) {
-        const uint32_t c = hist[b];
-        if (c) atomicAdd(&a.hist0[b], (unsigned long long)c);
-        a.offs0[u * f + b] = lookback(a.lb0, u, 0, f, b, c);
-    }
 }
 
 // Round-1 units: a bucket of h keys is cut into nu = max(1, round(h / C1))
@@ -530,8 +535,12 @@ static void set_smem(K k, size_t bytes) {
 
 void launch_count0(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(Count0Smem);
-    if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<a.U0, 512, sm, st>>>(a); }
-    else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<a.U0, 512, sm, st>>>(a); }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = a.U0 < 2u * (uint32_t)sms ? a.U0 : 2u * (unsigned)sms;  // persistent, 2 per SM
+    if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<g, 512, sm, st>>>(a); }
+    else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<g, 512, sm, st>>>(a); }
 }
 void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st) { k_plan0<<<1, 1024, 0, st>>>(a, dS_B); }
 void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
