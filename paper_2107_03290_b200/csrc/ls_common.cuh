@@ -160,9 +160,13 @@ __device__ __forceinline__ uint32_t sub_bucket_at(double xc, const Root &R, cons
 // Grid cell of a key for the b0 search (monotone in ord).
 template <int DT>
 __device__ __forceinline__ int b0_cell(uint64_t bits, double xmin, double xmax, double cs) {
-    const double xc = clampd(xd<DT>(bits), xmin, xmax);
-    const double r = __dmul_rn(__dsub_rn(xc, xmin), cs);
-    return (r < (double)(B0_CELLS - 1)) ? (int)__double2ll_rz(r) : B0_CELLS - 1;
+    // = clamp to [xmin, xmax] first, then (r < CELLS-1 ? trunc r : CELLS-1): a key
+    // below xmin gets r <= 0 (cell 0), one above xmax r > (xmax - xmin) * cs,
+    // which is >= CELLS-1 (cell CELLS-1); a NaN r (inf * 0, degenerate grid)
+    // fails r > 0 (cell 0); the conversion saturates
+    (void)xmax;
+    const double r = __dmul_rn(__dsub_rn(xd<DT>(bits), xmin), cs);
+    return r > 0.0 ? min(__double2int_rz(r), B0_CELLS - 1) : 0;
 }
 
 // b0 of a key from the thresholds (thr, cell in shared memory); bit-identical
