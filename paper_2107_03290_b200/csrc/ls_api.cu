@@ -340,7 +340,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         launches += 3;
     }
     launch_b0_table(a.M, l.L, l.f, dt, st);
-    launches += 2;
+    launches += 3;
     tm.mark(LS_PHASE_FIT);
     launch_count0(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, st);
@@ -431,6 +431,11 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
         for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
         fprintf(stderr, "\ntasks: warp %u cta4096 %u cta2048 %u cta1024 %u windows %u large %u\n",
                 c.ntask, c.nctask, c.nctask2, c.nctask3, c.nwin, c.nlarge);
+        if (pend->model_dev) {
+            uint32_t ns = 0;
+            cudaMemcpy(&ns, &pend->model_dev->nsub, 4, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "b0 refined cells: %u\n", ns);
+        }
     }
     if (c.status & STATUS_NAN) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
     if (c.status & STATUS_INTERNAL) { set_error("internal invariant violated (corrupt partition state)"); return LS_E_INTERNAL; }

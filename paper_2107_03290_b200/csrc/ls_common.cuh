@@ -60,6 +60,16 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 // arithmetic, one 2-byte and ~cnt 8-byte shared-memory loads instead of five
 // 8-byte leaf loads and the fp64 leaf line.
 constexpr int B0_CELLS = 16384;
+// Cells holding >= B0_SUBMIN thresholds (duplicate-heavy or very skewed
+// inputs: config 5's Zipf head puts ~350 of 999 thresholds into one cell) get
+// a refined grid of B0_SUB sub-cells (the grid at 64x the resolution: the
+// fine index trunc(64 r) is exact, 64 being a power of two), up to B0_NSUB such
+// cells. Cell entry count field: 0..61 exact, 62 = refined (offset field =
+// sub-grid number), 63 = more than 61 thresholds, not refined.
+constexpr int B0_SUB = 64;
+constexpr int B0_NSUB = 64;
+constexpr uint32_t B0_SUBMIN = 16;
+constexpr uint32_t B0_REFINED = 62, B0_SAT = 63;
 // Device copy of F_A. leaf[] holds (a, c, b, lo, hi) per leaf, 40 bytes.
 struct DevModel {
     double xmin, xmax, root_scale, last;  // last = (double)(L-1)
@@ -71,6 +81,9 @@ struct DevModel {
     uint32_t nthr, pad_;                      // valid thresholds: thr[0 .. nthr)
     unsigned long long thr[LS_MAX_FANOUT];    // thr[b-1] = min{o : b0(o) >= b}
     alignas(16) uint16_t cell[B0_CELLS];
+    alignas(16) uint16_t sub[B0_NSUB * B0_SUB];  // refined cells' sub-grids (same entry format)
+    uint16_t sub_cell[B0_NSUB];               // the cell of each sub-grid
+    uint32_t nsub;                            // refined cells (may exceed B0_NSUB: the rest stay B0_SAT)
 };
 
 // Root parameters held in registers (uniform across the grid).
@@ -169,6 +182,13 @@ __device__ __forceinline__ int b0_cell(uint64_t bits, double xmin, double xmax, 
     return r > 0.0 ? min(__double2int_rz(r), B0_CELLS - 1) : 0;
 }
 
+// Fine grid index (64 sub-cells per cell) of the same r: fine / 64 == b0_cell.
+template <int DT>
+__device__ __forceinline__ int b0_fine(uint64_t bits, double xmin, double cs) {
+    const double r = __dmul_rn(__dsub_rn(xd<DT>(bits), xmin), cs);
+    return r > 0.0 ? min(__double2int_rz(__dmul_rn(r, (double)B0_SUB)), B0_CELLS * B0_SUB - 1) : 0;
+}
+
 // b0 of a key from the thresholds (thr, cell in shared memory); bit-identical
 // to bucket0(predict(x)) by construction (see B0_CELLS).
 struct B0Search {
@@ -176,18 +196,26 @@ struct B0Search {
     uint32_t nthr;
     const unsigned long long *thr;
     const uint16_t *cell;
+    const uint16_t *sub;
     template <int DT>
     __device__ __forceinline__ uint32_t get(uint64_t bits) const {
         const int c = b0_cell<DT>(bits, xmin, xmax, cs);
-        const uint32_t e = cell[c];
+        uint32_t e = cell[c];
         uint32_t lo = e & 1023u, n = e >> 10;
         if (n == 0u) return lo;  // most keys: no threshold inside their cell
+        if (n == B0_REFINED) {   // dense cell: its sub-grid
+            e = sub[lo * B0_SUB + (b0_fine<DT>(bits, xmin, cs) - c * B0_SUB)];
+            lo = e & 1023u;
+            n = e >> 10;
+            if (n == 0u) return lo;
+        }
         const unsigned long long o = to_ord<DT>(bits);
         if (n == 1u) return lo + (thr[lo] <= o ? 1u : 0u);
-        if (n == 63u) {
+        if (n == B0_SAT) {
             // saturated count: the thresholds of cell c end where the next
             // cell's begin (its offset, when that cell owns ords at all)
-            const uint32_t nx = c + 1 < B0_CELLS ? (cell[c + 1] & 1023u) : 0u;
+            const uint32_t en = c + 1 < B0_CELLS ? cell[c + 1] : 0u;
+            const uint32_t nx = (en >> 10) == B0_REFINED ? 0u : (en & 1023u);  // (refined: a sub-grid number)
             n = (nx >= lo + 63u ? nx : nthr) - lo;
         }
         while (n > 0) {

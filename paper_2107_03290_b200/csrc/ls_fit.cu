@@ -234,21 +234,76 @@ __global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
             end = lo;
         }
         const uint32_t cnt = end - off;
-        entry = off | ((cnt < 63u ? cnt : 63u) << 10);
+        entry = off | ((cnt < B0_REFINED ? cnt : B0_SAT) << 10);
+        if (cnt >= B0_SUBMIN) {  // dense cell: refined by k_b0_sub if a sub-grid is left
+            const uint32_t k = atomicAdd(&M->nsub, 1u);
+            if (k < (uint32_t)B0_NSUB) {
+                M->sub_cell[k] = (uint16_t)c;
+                entry = k | (B0_REFINED << 10);
+            }
+        }
     }
     M->cell[c] = (uint16_t)entry;
+}
+
+// Sub-grids of the refined cells: entry (s) of sub-grid k covers the ords whose
+// fine index is 64 * sub_cell[k] + s, encoded like a cell entry (0..61 exact,
+// B0_SAT above). One thread per (k, s).
+template <int DT>
+__global__ void __launch_bounds__(256) k_b0_sub(DevModel *M) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t k = (uint32_t)t / B0_SUB, sidx = (uint32_t)t % B0_SUB;
+    if (k >= min(M->nsub, (uint32_t)B0_NSUB)) return;
+    const int fc = (int)M->sub_cell[k] * B0_SUB + (int)sidx;  // fine index of this sub-cell
+    const double xmin = M->xmin, cs = M->cell_scale;
+    unsigned long long omin, omax;
+    ord_domain<DT>(omin, omax);
+    auto first_ge = [&](int target, bool &none) {
+        unsigned long long lo = omin, hi = omax;
+        none = b0_fine<DT>(from_ord<DT>(hi), xmin, cs) < target;
+        while (lo < hi) {
+            const unsigned long long mid = lo + (hi - lo) / 2;
+            if (b0_fine<DT>(from_ord<DT>(mid), xmin, cs) >= target) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    bool none0, none1;
+    const unsigned long long s = first_ge(fc, none0);
+    const unsigned long long e = fc + 1 < B0_CELLS * B0_SUB ? first_ge(fc + 1, none1) : (none1 = true, 0ull);
+    uint32_t entry = 0;
+    if (!none0 && (none1 || e > s)) {  // sub-cell owns ords [s, o_hi]
+        const unsigned long long o_hi = none1 ? omax : e - 1;
+        const uint32_t V = M->nthr;
+        uint32_t off = 0, end = 0;  // #thr < s, #thr <= o_hi
+        for (uint32_t lo = 0, n = V; n > 0;) {
+            const uint32_t h = n >> 1;
+            if (M->thr[lo + h] < s) { lo += h + 1; n -= h + 1; } else n = h;
+            off = lo;
+        }
+        for (uint32_t lo = 0, n = V; n > 0;) {
+            const uint32_t h = n >> 1;
+            if (M->thr[lo + h] <= o_hi) { lo += h + 1; n -= h + 1; } else n = h;
+            end = lo;
+        }
+        const uint32_t cnt = end - off;
+        entry = off | ((cnt < B0_REFINED ? cnt : B0_SAT) << 10);
+    }
+    M->sub[k * B0_SUB + sidx] = (uint16_t)entry;
 }
 
 void launch_b0_table(DevModel *M, int L, int f, int dtype, cudaStream_t st) {
     (void)L;
     cudaMemsetAsync(&M->nthr, 0, sizeof(uint32_t), st);
+    cudaMemsetAsync(&M->nsub, 0, sizeof(uint32_t), st);
     const int g = (f + 255) / 256;
     if (dtype == DT_F64) {
         k_b0_thresholds<DT_F64><<<g, 256, 0, st>>>(M, f);
         k_b0_cells<DT_F64><<<B0_CELLS / 256, 256, 0, st>>>(M);
+        k_b0_sub<DT_F64><<<B0_NSUB * B0_SUB / 256, 256, 0, st>>>(M);
     } else {
         k_b0_thresholds<DT_U64><<<g, 256, 0, st>>>(M, f);
         k_b0_cells<DT_U64><<<B0_CELLS / 256, 256, 0, st>>>(M);
+        k_b0_sub<DT_U64><<<B0_NSUB * B0_SUB / 256, 256, 0, st>>>(M);
     }
 }
 

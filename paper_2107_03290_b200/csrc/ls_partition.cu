@@ -67,6 +67,7 @@ struct ModelBucket {
 struct alignas(16) B0Smem {
     unsigned long long thr[LS_MAX_FANOUT];
     uint16_t cell[B0_CELLS];
+    alignas(16) uint16_t sub[B0_NSUB * B0_SUB];
 };
 
 __device__ __forceinline__ B0Search load_b0_search(B0Smem &T, const DevModel *M) {
@@ -75,7 +76,11 @@ __device__ __forceinline__ B0Search load_b0_search(B0Smem &T, const DevModel *M)
     const uint4 *src = reinterpret_cast<const uint4 *>(M->cell);
     uint4 *dst = reinterpret_cast<uint4 *>(T.cell);
     for (int i = threadIdx.x; i < B0_CELLS / 8; i += blockDim.x) dst[i] = src[i];
-    return B0Search{M->xmin, M->xmax, M->cell_scale, V, T.thr, T.cell};
+    const uint32_t ns = min(M->nsub, (uint32_t)B0_NSUB);
+    const uint4 *ssrc = reinterpret_cast<const uint4 *>(M->sub);
+    uint4 *sdst = reinterpret_cast<uint4 *>(T.sub);
+    for (uint32_t i = threadIdx.x; i < ns * B0_SUB / 8; i += blockDim.x) sdst[i] = ssrc[i];
+    return B0Search{M->xmin, M->xmax, M->cell_scale, V, T.thr, T.cell, T.sub};
 }
 
 struct Count0Smem {

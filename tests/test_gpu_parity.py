@@ -139,8 +139,12 @@ def test_sort_bit_exact_1e6(dist):
     assert st["small_keys"] + st["big_keys"] + st["h1_keys"] + st["h0_keys"] <= 1_000_000
 
 
-@pytest.mark.parametrize("dist", ["normal", "lognormal", "zipf", "rootdups", "twodups", "telemetry"])
+@pytest.mark.parametrize("dist", ["normal", "lognormal", "zipf", "rootdups", "twodups", "telemetry",
+                                  "cfg5mix"])
 def test_sort_bit_exact_1e7(dist):
+    """(cfg5mix: the Zipf head packs hundreds of b0 thresholds into a few grid
+    cells, so the refined sub-grids of the b0 search are in use; S_B parity
+    checks every key's b0.)"""
     check_sort(gen(dist, 10_000_000, 11))
 
 
