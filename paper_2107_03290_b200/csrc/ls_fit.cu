@@ -175,9 +175,36 @@ __device__ __forceinline__ void ord_domain(unsigned long long &omin, unsigned lo
     omax = DT == DT_F64 ? 0xFFF0000000000000ull : ~0ull;  // ord(+inf)
 }
 
+// Smallest o in [lo, hi) with pred(o) true (pred monotone: false ... true),
+// else hi -- the bisection "while (lo < hi) { mid; pred(mid) ? hi = mid :
+// lo = mid + 1; }" run by a whole warp as a 33-ary search: each round the 32
+// lanes test 32 evenly spaced points and the ballot keeps the gap holding the
+// first true one (13 rounds over the 64-bit ord domain instead of 64).
+template <class P>
+__device__ __forceinline__ unsigned long long warp_first_true(const P &pred, unsigned long long lo,
+                                                             unsigned long long hi, int lane) {
+    while (hi - lo > 32) {
+        const unsigned long long step = (hi - lo) / 33;  // >= 1; 32 * step < hi - lo
+        const unsigned long long m = lo + step * (unsigned long long)(lane + 1);
+        const uint32_t bal = __ballot_sync(0xffffffffu, pred(m));
+        if (bal) {
+            const int f = __ffs(bal) - 1;
+            hi = lo + step * (unsigned long long)(f + 1);
+            lo = f == 0 ? lo : lo + step * (unsigned long long)f + 1;
+        } else {
+            lo = lo + step * 32ull + 1;
+        }
+    }
+    const unsigned long long m = lo + (unsigned long long)lane;
+    const uint32_t bal = __ballot_sync(0xffffffffu, m < hi && pred(m));
+    return bal ? lo + (unsigned long long)(__ffs(bal) - 1) : hi;
+}
+
+// one warp per threshold b = 1 .. f-1
 template <int DT>
 __global__ void __launch_bounds__(256) k_b0_thresholds(DevModel *M, int f) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int lane = threadIdx.x & 31;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) / 32 + 1;
     const Root R = load_root(M);
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         const double range = __dsub_rn(M->xmax, M->xmin);
@@ -188,17 +215,18 @@ __global__ void __launch_bounds__(256) k_b0_thresholds(DevModel *M, int f) {
     ord_domain<DT>(lo, hi);
     const double F = (double)f;
     if (b0_at<DT>(hi, R, M->leaf, F, f) < (uint32_t)b) {
-        M->thr[b - 1] = ~0ull;  // never reached: not counted in nthr
+        if (lane == 0) M->thr[b - 1] = ~0ull;  // never reached: not counted in nthr
         return;
     }
-    while (lo < hi) {
-        const unsigned long long mid = lo + (hi - lo) / 2;
-        if (b0_at<DT>(mid, R, M->leaf, F, f) >= (uint32_t)b) hi = mid; else lo = mid + 1;
+    const unsigned long long t = warp_first_true(
+        [&](unsigned long long o) { return b0_at<DT>(o, R, M->leaf, F, f) >= (uint32_t)b; }, lo, hi, lane);
+    if (lane == 0) {
+        M->thr[b - 1] = t;
+        atomicMax(&M->nthr, (uint32_t)b);
     }
-    M->thr[b - 1] = lo;
-    atomicMax(&M->nthr, (uint32_t)b);
 }
 
+// one thread per grid cell (16K cells: parallel enough for plain bisection)
 template <int DT>
 __global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -295,7 +323,7 @@ void launch_b0_table(DevModel *M, int L, int f, int dtype, cudaStream_t st) {
     (void)L;
     cudaMemsetAsync(&M->nthr, 0, sizeof(uint32_t), st);
     cudaMemsetAsync(&M->nsub, 0, sizeof(uint32_t), st);
-    const int g = (f + 255) / 256;
+    const int g = (f * 32 + 255) / 256;  // k_b0_thresholds: one warp per threshold
     if (dtype == DT_F64) {
         k_b0_thresholds<DT_F64><<<g, 256, 0, st>>>(M, f);
         k_b0_cells<DT_F64><<<B0_CELLS / 256, 256, 0, st>>>(M);
