@@ -26,20 +26,21 @@ namespace ls {
 constexpr int TP_THREADS = 1024;
 constexpr int TP_KPT = 8;
 constexpr int TP_TILE = TP_THREADS * TP_KPT;  // 8192 keys
+constexpr int TP_NSLOT = 2;                   // ring slots (3 slots of 6K-key tiles measured slower: shorter runs)
 constexpr int TP_SLOT = TP_TILE + 2;          // + aligned-hull slack
 
 constexpr size_t MAX_SMEM_OPTIN = 232448;  // 227 KB per block on sm_100
-typedef uint16_t TpBids[2][TP_TILE + 16];  // staged precomputed bucket ids (BIDS mode)
+typedef uint16_t TpBids[TP_NSLOT][TP_TILE + 16];  // staged precomputed bucket ids (BIDS mode)
 
 struct TpSmem {
-    uint64_t ring[2][TP_SLOT];
+    uint64_t ring[TP_NSLOT][TP_SLOT];
     uint16_t sbin[TP_TILE];
     uint32_t cnt[LS_MAX_FANOUT];
     uint32_t ex[LS_MAX_FANOUT];
     uint32_t delta[LS_MAX_FANOUT];
     uint32_t wsum[33];
     uint32_t tot;
-    uint64_t mbar[2];
+    uint64_t mbar[TP_NSLOT];
 };
 
 constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (SKIP mode)
@@ -96,16 +97,14 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
     if (ntl == 0) return;
-    if (tid == 0) {
-        tp_issue(S, 0, src, beg, umin64(end, beg + TP_TILE), len, BIDS ? bid : nullptr, sb);
-        if (ntl > 1)
-            tp_issue(S, 1, src, beg + TP_TILE, umin64(end, beg + 2 * TP_TILE), len, BIDS ? bid : nullptr,
-                     sb);
-    }
+    if (tid == 0)
+        for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && j < ntl; j++)
+            tp_issue(S, (int)j, src, beg + j * TP_TILE, umin64(end, beg + (j + 1) * TP_TILE), len,
+                     BIDS ? bid : nullptr, sb);
     if (tid < nb) S.cnt[tid] = 0;
     __syncthreads();
     for (uint64_t i = 0; i < ntl; i++) {
-        const int slot = (int)(i & 1);
+        const int slot = (int)(i % TP_NSLOT);
         const uint64_t t0 = beg + i * TP_TILE;
         const int tn = (int)umin64((uint64_t)TP_TILE, end - t0);
         mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
@@ -187,17 +186,16 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         __syncthreads();
         mark(4);
         phase ^= 1u << slot;
-        if (tid == 0 && i + 2 < ntl)
-            tp_issue(S, slot, src, t0 + 2 * TP_TILE, umin64(end, t0 + 3 * TP_TILE), len,
+        if (tid == 0 && i + TP_NSLOT < ntl)
+            tp_issue(S, slot, src, t0 + (uint64_t)TP_NSLOT * TP_TILE,
+                     umin64(end, t0 + (uint64_t)(TP_NSLOT + 1) * TP_TILE), len,
                      BIDS ? bid : nullptr, sb);
     }
 }
 
 __device__ __forceinline__ void tp_init(TpSmem &S) {
-    if (threadIdx.x == 0) {
-        mbar_init(&S.mbar[0], 1);
-        mbar_init(&S.mbar[1], 1);
-    }
+    if (threadIdx.x == 0)
+        for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.mbar[j], 1);
     __syncthreads();
 }
 
