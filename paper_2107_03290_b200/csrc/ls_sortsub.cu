@@ -1379,19 +1379,51 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
         }
         __syncthreads();
         BG_PROF(1);
+        // a digit holding >= 1/16 of the item (a heavy duplicate): the scatter
+        // aggregates equal digits per warp instruction (one counter update per
+        // digit, and the group's keys land contiguously) instead of letting
+        // up to 32 lanes serialise on one counter
+        {
+            uint32_t m = 0;
+            for (int d = tid; d < BIG_DIGITS; d += bd) m = max(m, S.start[d]);
+            m = __reduce_max_sync(0xffffffffu, m);
+            if (tid == 0) S.tmp[35] = 0;
+            __syncthreads();
+            if (lane == 0) atomicMax(&S.tmp[35], m);
+            __syncthreads();
+        }
+        const bool agg = S.tmp[35] * 16u >= item.size;
         block_exscan(S.start, BIG_DIGITS, S.tmp);
         for (int d = tid; d < BIG_DIGITS; d += bd) S.end[d] = S.start[d];
         __syncthreads();
-        for (uint32_t i = tid; i < item.size; i += 4 * bd) {
+        if (!agg) {
+            for (uint32_t i = tid; i < item.size; i += 4 * bd) {
+                uint64_t v[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) v[q] = (i + q * bd < item.size) ? X[i + q * bd] : 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (i + q * bd < item.size) {
+                        const uint32_t d = (uint32_t)((to_ord<DT>(v[q]) - mn) >> shift);
+                        Y[atomicAdd(&S.end[d], 1u)] = v[q];
+                    }
+            }
+        } else for (uint32_t i0 = (uint32_t)(tid & ~31); i0 < item.size; i0 += 4 * bd) {
+            const uint32_t i = i0 + (uint32_t)lane;  // (warp-uniform bound for the match)
             uint64_t v[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) v[q] = (i + q * bd < item.size) ? X[i + q * bd] : 0;
 #pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (i + q * bd < item.size) {
-                    const uint32_t d = (uint32_t)((to_ord<DT>(v[q]) - mn) >> shift);
-                    Y[atomicAdd(&S.end[d], 1u)] = v[q];
-                }
+            for (int q = 0; q < 4; q++) {
+                const bool ok = i + q * bd < item.size;
+                const uint32_t d = ok ? (uint32_t)((to_ord<DT>(v[q]) - mn) >> shift) : 0xffffffffu;
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                const int leader = __ffs(peers) - 1;
+                uint32_t at = 0;
+                if (ok && lane == leader) at = atomicAdd(&S.end[d], (uint32_t)__popc(peers));
+                at = __shfl_sync(0xffffffffu, at, leader) + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+                if (ok) Y[at] = v[q];  // peers land contiguously
+            }
         }
         __syncthreads();  // S.end[d] = end of piece d; Y holds the pieces
         BG_PROF(2);
