@@ -849,6 +849,7 @@ struct CsSmem {
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
     uint32_t nbig, ovf, mgs, mgx;   // mgx: a group > 8 keys outside slot n'-1
+    uint32_t huge[16], nhuge;       // listed groups of > 256 keys (<= CS_MAX / 257 of them)
     unsigned long long st[5];
 };
 
@@ -900,7 +901,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
-        if (tid == 0) S.nbig = S.ovf = S.mgs = S.mgx = 0;
+        if (tid == 0) S.nbig = S.ovf = S.mgs = S.mgx = S.nhuge = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
@@ -1078,7 +1079,10 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     if (S.K[sl + 1] - S.K[sl] < 2u) continue;
                 }
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
-                if (c > 256u && k < nb) continue;  // the whole CTA sorts it below
+                if (c > 256u && k < nb) {  // the whole CTA sorts it below
+                    if (lane == 0) S.huge[atomicAdd(&S.nhuge, 1u)] = sl;
+                    continue;
+                }
                 if (c <= BS_RANKMAX) {
                     if (lane == 0) {
                         for (uint32_t x = 1; x < c; x++) {
@@ -1117,10 +1121,10 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             __syncthreads();
             // listed groups of > 256 keys (duplicate-heavy inputs): shared-
             // memory bitonic by all threads, one group at a time
-            for (uint32_t k = 0; k < nb; k++) {
-                const uint32_t sl = S.big[k];
+            const uint32_t nh = S.nhuge;
+            for (uint32_t k = 0; k < nh; k++) {
+                const uint32_t sl = S.huge[k];
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
-                if (c <= 256u) continue;
                 if (has_big) {
                     if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
                 } else {
