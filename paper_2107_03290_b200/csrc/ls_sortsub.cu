@@ -843,12 +843,11 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 template <int CAP>
 struct CsSmem {
     uint64_t T[CAP + CAP / 8];
-    uint32_t mixed[CAP / 32];               // per pos: its group holds >= 2 distinct keys
     alignas(16) uint32_t K[CAP + 8];
     uint16_t slot_of[CAP];
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
-    uint32_t nbig, ovf, mgs, mgx;   // mgx: a group > 8 keys outside slot n'-1
+    uint32_t nbig, ovf, mgs;
     uint32_t huge[16], nhuge;       // listed groups of > 256 keys (<= CS_MAX / 257 of them)
     unsigned long long st[5];
 };
@@ -901,7 +900,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
-        if (tid == 0) S.nbig = S.ovf = S.mgs = S.mgx = S.nhuge = 0;
+        if (tid == 0) S.nbig = S.ovf = S.mgs = S.nhuge = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
@@ -943,7 +942,6 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 if (c > BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
-                    if (idx != np - 1u) S.mgx = 1u;  // a big group other than R5's end pile-up
                 }
                 sum += c;
             }
@@ -967,15 +965,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         __syncthreads();
-        // placement. With a group of > 8 keys in any slot but the
-        // last (duplicate-heavy inputs) all threads flag the mixed-value
-        // groups in the touch-up, so that the group sorts skip one-value
-        // groups without a serial scan. A big group in slot n'-1 alone is the
-        // pile-up of R5's clamp when n' < n / f^2 (smooth inputs at n ~ 10^9):
-        // its warp checks it.
-        const bool has_big = S.mgx != 0;
-        if (has_big)
-            for (uint32_t i = tid; i < (np + 31) / 32; i += CS_THREADS) S.mixed[i] = 0;
+        // placement
 #pragma unroll
         for (int k = 0; k < CS_KPT; k++) {
             if (code[k] != BS_NONE) {
@@ -995,42 +985,12 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         for (int half = 0; half < (CS_KPT > 8 && np > 8u * CS_THREADS ? 2 : 1); half++) {
             const uint32_t row_i = (uint32_t)(half * CS_THREADS + tid);  // row of 8 positions
             const uint32_t q0 = 8u * row_i;
-            if (iters > 0 || has_big) {
+            if (iters > 0) {
                 uint64_t v[8];
                 {
                     const uint64_t *row = S.T + 9u * row_i;
 #pragma unroll
                     for (int q = 0; q < 8; q++) v[q] = q0 + q < np ? row[q] : ~0ull;
-                }
-                if (has_big) {
-                    // mixed-group flags: equal-slot neighbours with different
-                    // keys (the pair across two rows from the row on the left;
-                    // shared memory at warp boundaries)
-                    const uint2 s2 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i];
-                    const uint2 s3 = reinterpret_cast<const uint2 *>(S.slot_of)[2 * row_i + 1];
-                    const uint32_t sw[4] = {s2.x, s2.y, s3.x, s3.y};
-                    uint32_t sv[8];
-#pragma unroll
-                    for (int q = 0; q < 8; q++)
-                        sv[q] = q0 + q < np ? ((sw[q >> 1] >> (16 * (q & 1))) & 0xffffu) : 0x10000u + q;
-                    uint64_t nv0 = __shfl_down_sync(0xffffffffu, v[0], 1);
-                    uint32_t ns0 = __shfl_down_sync(0xffffffffu, sv[0], 1);
-                    if (lane == 31) {
-                        const uint32_t qn = q0 + 8u;
-                        if (qn < np) {
-                            nv0 = S.T[9u * (row_i + 1u)];
-                            ns0 = S.slot_of[qn];
-                        } else {
-                            ns0 = 0xfffffu;
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        const uint64_t y = q < 7 ? v[q + 1] : nv0;
-                        const uint32_t sy = q < 7 ? sv[q + 1] : ns0;
-                        if (sv[q] < 0x10000u && sv[q] == sy && v[q] != y)
-                            atomicOr(&S.mixed[sv[q] >> 5], 1u << (sv[q] & 31u));
-                    }
                 }
                 auto pass = [&](bool track) -> bool {
                     uint32_t moved = 0;
@@ -1097,13 +1057,9 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     }
                     continue;
                 }
-                if (has_big) {
-                    if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
-                } else {
-                    bool same = true;
-                    for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
-                    if (__all_sync(0xffffffffu, same)) continue;
-                }
+                bool same = true;  // one value (duplicate-heavy inputs): nothing to do
+                for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
+                if (__all_sync(0xffffffffu, same)) continue;
                 if (c <= 32u) {
                     uint64_t v1 = (uint32_t)lane < c ? T[base + lane] : ~0ull;
                     warp_sort32(v1, lane);
@@ -1125,13 +1081,9 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             for (uint32_t k = 0; k < nh; k++) {
                 const uint32_t sl = S.huge[k];
                 const uint32_t base = S.K[sl], c = S.K[sl + 1] - base;
-                if (has_big) {
-                    if (!((S.mixed[sl >> 5] >> (sl & 31u)) & 1u)) continue;  // one value
-                } else {
-                    bool diff = false;
-                    for (uint32_t q = tid; q < c; q += CS_THREADS) diff |= (T[base + q] != T[base]);
-                    if (!__syncthreads_or(diff)) continue;
-                }
+                bool diff = false;  // one value: nothing to do
+                for (uint32_t q = tid; q < c; q += CS_THREADS) diff |= (T[base + q] != T[base]);
+                if (!__syncthreads_or(diff)) continue;
                 bitonic_view<PadT, true>(T + base, (int)c, tid, CS_THREADS);
             }
         }
