@@ -371,10 +371,8 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     launches++;
     launch_large(a, dt, st);
     launches += 5;
-    for (int lv = 0; lv < BIG_LEVELS; lv++) {
-        launch_big(a, lv, dt, st);
-        launches++;
-    }
+    launch_big(a, dt, st);
+    launches++;
     tm.mark(LS_PHASE_BIG);
     LS_CUDA(cudaGetLastError());
     pend->ctl_dev = a.ctl;

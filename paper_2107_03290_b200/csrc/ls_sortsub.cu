@@ -13,8 +13,12 @@
 // radix partition on ord(x) - ord(min) (12-bit digits aligned to the key
 // range) into the scratch copy, then every piece is sorted in shared memory;
 // pieces larger than the shared-memory sort capacity go to the next level.
+#include <cooperative_groups.h>
+
 #include "ls_launch.h"
 #include "ls_warpsort.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ls {
 
@@ -1248,17 +1252,11 @@ struct BigSmem {
 // one warp per larger piece (bitonic). Pieces in (BIG_CHUNK, BIG_SORT_CAP]
 // are block-sorted; larger ones become items of the next level.
 template <int DT>
-__global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
-    if (a.ctl->status) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    BigSmem &S = *reinterpret_cast<BigSmem *>(smem_raw);
+__device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, uint32_t &mphase) {
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
-    const uint32_t cnt = min(a.ctl->big_cnt[level], a.big_cap);
+    const uint32_t cnt = min(*(volatile uint32_t *)&a.ctl->big_cnt[level], a.big_cap);
     const BigItem *list = a.big + (size_t)level * a.big_cap;
-    uint32_t mphase = 0;
-    if (tid == 0) mbar_init(&S.mbar, 1);
-    __syncthreads();
     const bool prof = (a.dbg & 512u) && threadIdx.x == 0;
     long long t_prev = clock64();
 #define BG_PROF(k)                                                                  \
@@ -1516,6 +1514,25 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a, int level) {
     }
 }
 
+// All big-path levels in one cooperative launch: level l + 1's items are
+// complete after a grid barrier; the kernel stops at the first empty level
+// (for smooth inputs: at once), instead of BIG_LEVELS separate launches.
+template <int DT>
+__global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a) {
+    if (a.ctl->status) return;  // (set before this kernel: uniform across the grid)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BigSmem &S = *reinterpret_cast<BigSmem *>(smem_raw);
+    uint32_t mphase = 0;
+    if (threadIdx.x == 0) mbar_init(&S.mbar, 1);
+    __syncthreads();
+    cg::grid_group grid = cg::this_grid();
+    for (int lv = 0; lv < BIG_LEVELS; lv++) {
+        if (*(volatile uint32_t *)&a.ctl->big_cnt[lv] == 0) break;  // uniform: read after a grid barrier
+        big_level<DT>(a, lv, S, mphase);
+        grid.sync();
+    }
+}
+
 // -------------------------------------------------------------- launchers --
 template <int NT, int KPT, int PER_SM>
 static void launch_ctasort(const Args &a, int dtype, cudaStream_t st, const uint4 *list,
@@ -1563,16 +1580,18 @@ void launch_big_minmax(const Args &a, int dtype, cudaStream_t st) {
     else k_big_minmax<DT_U64><<<148 * 4, 512, 0, st>>>(a);
 }
 
-void launch_big(const Args &a, int level, int dtype, cudaStream_t st) {
+void launch_big(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(BigSmem);
-    const int grid = 148 * 2;
-    if (dtype == DT_F64) {
-        cudaFuncSetAttribute(k_big<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_big<DT_F64><<<grid, BIG_THREADS, sm, st>>>(a, level);
-    } else {
-        cudaFuncSetAttribute(k_big<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_big<DT_U64><<<grid, BIG_THREADS, sm, st>>>(a, level);
-    }
+    int dev = 0, sms = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    void *fn = dtype == DT_F64 ? (void *)k_big<DT_F64> : (void *)k_big<DT_U64>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, BIG_THREADS, sm);
+    dim3 grid((unsigned)(sms * (per < 2 ? (per < 1 ? 1 : per) : 2))), block(BIG_THREADS);
+    Args aa = a;
+    void *args[] = {&aa};
+    cudaLaunchCooperativeKernel(fn, grid, block, args, sm, st);
 }
 
 }  // namespace ls
