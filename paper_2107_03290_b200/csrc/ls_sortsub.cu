@@ -903,7 +903,8 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 continue;
             }
         }
-        for (uint32_t i = tid; i <= np; i += CS_THREADS) S.K[i] = 0;
+        for (uint32_t i = 4 * tid; i <= np; i += 4 * CS_THREADS)  // (K has CAP + 8 entries)
+            *reinterpret_cast<uint4 *>(&S.K[i]) = make_uint4(0, 0, 0, 0);
         if (tid == 0) S.nbig = S.ovf = S.mgs = S.nhuge = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
