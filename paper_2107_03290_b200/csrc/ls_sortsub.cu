@@ -1321,7 +1321,7 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
         const int bits = 64 - __clzll((long long)range);
         const int shift = bits > 12 ? bits - 12 : 0;
         for (int d = tid; d < BIG_DIGITS; d += bd) S.start[d] = 0;
-        if (tid == 0) S.nblk = 0;
+        if (tid == 0) S.nblk = S.nwbig = 0;
         __syncthreads();
         for (uint32_t i = tid; i < item.size; i += 4 * bd) {
             uint64_t v[4];
@@ -1444,7 +1444,6 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                         bulk_g2s((char *)S.sk + o, (const char *)(Yb + h0) + o,
                                  bytes - o < 32768u ? bytes - o : 32768u, &S.mbar);
                 }
-                if (tid == 0) S.nwbig = 0;
                 BG_PROF(5);
                 mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
@@ -1495,6 +1494,7 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                     bitonic<DT, true>(sk + (S.start[d] - slo), (int)(S.end[d] - S.start[d]), tid, bd);
                 }
                 BG_PROF(8);
+                if (tid == 0) S.nwbig = 0;  // for the next window (ordered by the barrier below)
                 for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
                 __syncthreads();
                 BG_PROF(9);
