@@ -64,9 +64,11 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.ntiles = (uint32_t)((n + l.T_tile - 1) / l.T_tile);
     if (l.ntiles == 0) l.ntiles = 1;
     const uint64_t ff = (uint64_t)l.f * l.f;
-    // big items per level: level 0 holds sub-buckets > T_small keys; deeper
-    // levels hold pieces > 256 keys (ls_bigpath.cu) or > BIG_SORT_CAP (k_big)
-    l.big_cap = (uint32_t)(n / 257 + 64);
+    // big items per level: level 0 holds the sub-buckets of > T_small keys (at most n / (T_small + 1)
+    // of them); deeper levels hold pieces of > 256 keys (ls_bigpath.cu) or
+    // > BIG_SORT_CAP keys (k_big): at most n / 257
+    const uint64_t tb = l.T_small < 256 ? l.T_small : 256;
+    l.big_cap = (uint32_t)(n / (tb + 1) + 64);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = align_up(off, 256);

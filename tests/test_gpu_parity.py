@@ -217,6 +217,20 @@ def test_sort_edge_cases(name):
         assert np.array_equal(bits(to_np(t)), bits(O.sort(h, cfg=ocfg)[0]))
 
 
+@pytest.mark.parametrize("dist,n,seed,kw", [
+    ("telemetry", 235_725, 439_674_140, dict(big_threshold=64)),
+    ("chisq4", 1_179_994, 516_369_813, dict(fanout=100, big_threshold=100)),
+    ("twodups", 992_914, 52_170_342, dict(fanout=100, big_threshold=64)),
+])
+def test_many_big_items(dist, n, seed, kw):
+    """Regressions from scripts/stress.py: with a small big threshold more
+    than n/257 sub-buckets become big items; the item lists are sized from the
+    threshold (n / (T + 1)), so no capacity error and the oracle's output."""
+    cfg = ls.config(**kw)
+    ocfg = O.config(fanout=kw.get("fanout", 1000))
+    check_sort(gen(dist, n, seed), cfg=cfg, ocfg=ocfg, f=kw.get("fanout", 1000))
+
+
 def test_misaligned_keys_rejected():
     """Keys at an odd 8-byte offset (a tensor slice) are rejected before any
     work, as include/ls.h states: the TMA stages address aligned key pairs."""
