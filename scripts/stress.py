@@ -51,15 +51,37 @@ def main():
             os.environ["LS_FR_MIN"] = str(int(rng.choice([256, 4096, 65536])))
         else:
             os.environ.pop("LS_FR_MIN", None)
-        try:
-            plan = datagen.Plan(dist, n, seed)
-        except Exception:  # (generator limits, e.g. twodups n < 2^32)
-            continue
-        tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
-        t = torch.empty(n, dtype=tdt, device="cuda")
-        if n:
-            plan.device(t)
-        h = t.view(torch.int64).cpu().numpy().view(np.uint64).view(plan.dtype).copy()
+        if rng.random() < 0.25:  # host-made patterns: order, few values, clusters, specials
+            pat = int(rng.integers(7))
+            r2 = np.random.default_rng(seed)
+            if pat == 0:
+                h = np.sort(r2.standard_normal(n))
+            elif pat == 1:
+                h = np.sort(r2.standard_normal(n))[::-1].copy()
+            elif pat == 2:
+                h = np.full(n, r2.standard_normal())
+            elif pat == 3:
+                h = r2.integers(0, int(r2.integers(1, 17)), n).astype(np.uint64)
+            elif pat == 4:
+                h = (r2.integers(0, 4, n) * 1e6 + r2.integers(0, 1000, n) * 1e-9).astype(np.float64)
+            elif pat == 5:
+                sp = np.array([np.inf, -np.inf, 0.0, -0.0, 5e-324, -5e-324, 1e308, -1e308])
+                h = np.where(r2.random(n) < 0.3, sp[r2.integers(0, len(sp), n)], r2.standard_normal(n))
+            else:
+                h = (np.uint64(1) << np.uint64(63)) + r2.integers(0, 2 ** 20, n).astype(np.uint64)
+            dist = f"pattern{pat}"
+            tdt = torch.float64 if h.dtype == np.float64 else torch.uint64
+            t = torch.from_numpy(h.view(np.int64).copy()).cuda().view(tdt)
+        else:
+            try:
+                plan = datagen.Plan(dist, n, seed)
+            except Exception:  # (generator limits, e.g. twodups n < 2^32)
+                continue
+            tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
+            t = torch.empty(n, dtype=tdt, device="cuda")
+            if n:
+                plan.device(t)
+            h = t.view(torch.int64).cpu().numpy().view(np.uint64).view(plan.dtype).copy()
         try:
             ls.ls_sort(t, cfg=ls.config(**kw))
             got = t.view(torch.int64).cpu().numpy().view(np.uint64)
