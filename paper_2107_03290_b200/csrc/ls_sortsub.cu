@@ -686,12 +686,11 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         {
             constexpr int PER = 9;
             uint32_t v[PER];
-            uint32_t sum = 0, mg = 0, bigm = 0;
+            uint32_t sum = 0, bigm = 0;
 #pragma unroll
             for (int q = 0; q < PER; q++) {
                 const uint32_t idx = PER * lane + q;
                 const uint32_t c = idx < np ? W.K[idx] : 0u;
-                mg = c > mg ? c : mg;
                 mgs = (c <= BS_RANKMAX && c > mgs) ? c : mgs;
                 bigm |= (c > BS_RANKMAX ? 1u : 0u) << q;
                 v[q] = sum;
@@ -704,9 +703,8 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 const uint32_t idx = PER * lane + q;
                 if (idx <= np) W.K[idx] = v[q] + off;
             }
-            mg = __reduce_max_sync(0xffffffffu, mg);
             mgs = __reduce_max_sync(0xffffffffu, mgs);
-            r_maxg = mg > r_maxg ? mg : r_maxg;
+            r_maxg = mgs > r_maxg ? mgs : r_maxg;  // (groups > 8: in the loop below)
             // list the groups > 8 (pos values) for the warp sorts below
             const uint32_t nbl = __popc(bigm);
             const uint32_t pre = warp_incl_scan(nbl) - nbl;
@@ -788,6 +786,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                         if (W.K[x + 1] - W.K[x] > BS_RANKMAX && seen++ == k) { pos = x; break; }
                 }
                 const uint32_t base = W.K[pos], c = W.K[pos + 1] - base;
+                r_maxg = c > r_maxg ? c : r_maxg;
                 bool same = true;
                 for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
                 if (__all_sync(0xffffffffu, same)) continue;
