@@ -609,10 +609,12 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     if (a.ctl->status) return;
     __shared__ WsSlice SL[WS_WARPS];
     __shared__ unsigned long long st_red[4];
+    __shared__ uint32_t wst[WS_WARPS][4];  // per warp: small / small keys / H1 / H1 keys (off the registers)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WsSlice &W = SL[warp];
     const PadT T{W.T, 0u};
     if (threadIdx.x < 4) st_red[threadIdx.x] = 0;
+    if (threadIdx.x < 4 * WS_WARPS) (&wst[0][0])[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t ntask = min(a.ctl->ntask, a.task_cap);
     if (blockIdx.x * WS_WARPS >= ntask) return;  // (no task for this block: skip the model reads)
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t nw = gridDim.x * WS_WARPS;
-    uint32_t r_small = 0, r_smallk = 0, r_h1 = 0, r_h1k = 0, r_maxg = 0;
+    uint32_t r_maxg = 0;
     uint4 nxt = blockIdx.x * WS_WARPS + warp < ntask ? a.tasks[blockIdx.x * WS_WARPS + warp]
                                                        : make_uint4(0, 0, 0, 0);
     for (uint32_t t = blockIdx.x * WS_WARPS + warp; t < ntask; t += nw) {
@@ -643,8 +645,10 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             }
             if (!__any_sync(0xffffffffu, diff)) {
                 if (lane == 0 && a.dH1) a.dH1[g] = 1;
-                r_h1++;
-                r_h1k += np;
+                if (lane == 0) {
+                    wst[warp][2]++;
+                    wst[warp][3] += np;
+                }
                 continue;
             }
         }
@@ -810,20 +814,22 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 #pragma unroll
             for (int k = 0; k < WS_KPL; k++)
                 if (32u * k + lane < np) gl[32 * k] = from_ord<DT>(tl[36 * k]);
-            r_small++;
-            r_smallk += np;
+            if (lane == 0) {
+                wst[warp][0]++;
+                wst[warp][1] += np;
+            }
         } else {
             if (lane == 0 && a.dH1) a.dH1[g] = 1;
-            r_h1++;
-            r_h1k += np;
+            if (lane == 0) {
+                wst[warp][2]++;
+                wst[warp][3] += np;
+            }
         }
         __syncwarp();
     }
     if (lane == 0) {
-        if (r_small) atomicAdd(&st_red[0], (unsigned long long)r_small);
-        if (r_smallk) atomicAdd(&st_red[1], (unsigned long long)r_smallk);
-        if (r_h1) atomicAdd(&st_red[2], (unsigned long long)r_h1);
-        if (r_h1k) atomicAdd(&st_red[3], (unsigned long long)r_h1k);
+        for (int q = 0; q < 4; q++)
+            if (wst[warp][q]) atomicAdd(&st_red[q], (unsigned long long)wst[warp][q]);
         if (r_maxg > 1) atomicMax(&a.ctl->stat[ST_MAXGRP], (unsigned long long)r_maxg);
     }
     __syncthreads();
