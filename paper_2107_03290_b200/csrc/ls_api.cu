@@ -6,7 +6,9 @@
 #include <string.h>
 
 #include <memory>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "ls.h"
 #include "ls_api_internal.h"
@@ -284,47 +286,13 @@ struct Timer {
     }
 };
 
-// Enqueue the whole sort. If `sync` the stream is synchronised and the status
-// and stats are collected; otherwise the caller synchronises (ls_sort_host).
-ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg_in,
-                       const ls_model *inject, void *d_ws, size_t ws_bytes, cudaStream_t st,
-                       ls_stats *stats, const ls_dumps *dumps, Pending *pend) {
-    ls_config cfg;
-    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
-    ls_status rc = check_config(cfg);
-    if (rc != LS_OK) return rc;
-    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
-    if (n >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
-    if (stats) memset(stats, 0, sizeof *stats);
-    if (stats) stats->n = n;
-    if (n <= 1) return LS_OK;
-    if (!d_keys || !d_ws) { set_error("null pointer"); return LS_E_INVALID; }
-    // the bulk-copy (TMA) stages and 16-byte vector loads address keys in aligned pairs
-    if (((uintptr_t)d_keys & 15) || ((uintptr_t)d_ws & 255)) {
-        set_error("keys must be 16-byte aligned and the workspace 256-byte aligned");
-        return LS_E_INVALID;
-    }
-    if (inject && !model_ok(*inject, cfg)) { set_error("injected model is not monotone-safe"); return LS_E_INVALID; }
-    const Layout l = make_layout(n, cfg);
-    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
-    Args a = make_args(l, d_keys, d_ws);
-    if (const char *e = getenv("LS_DEBUG_STAGE")) a.dbg = (uint32_t)atoi(e);
-    // cluster-resident round 1 (SURVEY f2) with LS_FLAG_FUSED_ROUND1; LS_FR_MIN
-    // overrides the smallest bucket it takes (tests)
-    a.fr_cap = (cfg.flags & LS_FLAG_FUSED_ROUND1) ? round1_capacity() : 0u;
-    a.fr_min = a.fr_cap ? FR_MIN_DEFAULT : 0u;
-    if (const char *e = getenv("LS_FR_MIN")) a.fr_min = a.fr_cap ? (uint32_t)atoi(e) : 0u;
-    const int dt = (int)dtype;
+// The launch sequence of one sort, from the workspace initialisation to the
+// big path. Every data-dependent decision is taken on the device (task lists,
+// counters in Ctl), so the sequence depends only on its arguments.
+static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg, const ls_model *inject,
+                                 const ls_dumps *dumps, int dt, void *d_ws, Timer &tm, cudaStream_t st,
+                                 uint64_t &launches) {
     unsigned char *w = (unsigned char *)d_ws;
-    if (dumps) {
-        a.dH0 = dumps->d_H0;
-        a.dH1 = dumps->d_H1;
-        if (a.dH0) LS_CUDA(cudaMemsetAsync(a.dH0, 0, (size_t)l.f, st));
-        if (a.dH1) LS_CUDA(cudaMemsetAsync(a.dH1, 0, (size_t)l.f * l.f, st));
-    }
-    Timer tm;
-    tm.start(cfg.flags & LS_FLAG_PHASE_TIMING, st);
-    uint64_t launches = 0;
     LS_CUDA(cudaMemsetAsync(w + l.ff_begin, 0xff, l.ff_end - l.ff_begin, st));
     LS_CUDA(cudaMemsetAsync(w + l.zero_begin, 0, l.zero_end - l.zero_begin, st));
     launch_init(a, st);
@@ -377,6 +345,164 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     launches++;
     tm.mark(LS_PHASE_BIG);
     LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+// CUDA Graph of the launch sequence. A sort is captured the
+// second time the same (keys, n, dtype, config, workspace, device) comes back
+// (one-shot calls run the sequence directly) and replayed with one
+// cudaGraphLaunch from then on. Off with LS_GRAPH=0; LS_GRAPH=2 turns a failed
+// capture into an error (tests). Never with an injected model (host sync),
+// dumps or phase timing.
+struct GraphKey {
+    void *keys, *ws;
+    uint64_t n;
+    ls_config cfg;
+    int dt, dev;
+    uint32_t fr_min, dbg;
+};
+struct GraphEntry {
+    GraphKey k;
+    cudaGraphExec_t exec;  // null: seen once
+    uint64_t launches, used;
+};
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;
+static uint64_t g_graph_clock = 0;
+constexpr size_t GRAPH_CACHE = 16;
+
+static bool same_key(const GraphKey &x, const GraphKey &y) {
+    return x.keys == y.keys && x.ws == y.ws && x.n == y.n && x.dt == y.dt && x.dev == y.dev &&
+           x.fr_min == y.fr_min && x.dbg == y.dbg && !memcmp(&x.cfg, &y.cfg, sizeof x.cfg);
+}
+
+static bool graphs_enabled() {
+    const char *e = getenv("LS_GRAPH");
+    return !(e && e[0] == '0');
+}
+
+// Run the sequence through the graph cache; false = not handled (run it directly).
+static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt, const GraphKey &key,
+                         cudaStream_t st, uint64_t &launches, ls_status &rc) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphEntry *e = nullptr;
+    for (auto &g : g_graphs)
+        if (same_key(g.k, key)) e = &g;
+    if (!e) {  // first sight: remember it, run directly
+        if (g_graphs.size() >= GRAPH_CACHE) {
+            size_t lru = 0;
+            for (size_t i = 1; i < g_graphs.size(); i++)
+                if (g_graphs[i].used < g_graphs[lru].used) lru = i;
+            if (g_graphs[lru].exec) cudaGraphExecDestroy(g_graphs[lru].exec);  // (freed after in-flight launches)
+            g_graphs.erase(g_graphs.begin() + lru);
+        }
+        g_graphs.push_back(GraphEntry{key, nullptr, 0, ++g_graph_clock});
+        return false;
+    }
+    e->used = ++g_graph_clock;
+    if (!e->exec) {  // second sight: capture on a private stream
+        static thread_local cudaStream_t cs[64] = {};
+        if (key.dev < 0 || key.dev >= 64) return false;
+        if (!cs[key.dev] && cudaStreamCreateWithFlags(&cs[key.dev], cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (cudaStreamBeginCapture(cs[key.dev], cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        Timer off;
+        uint64_t nl = 0;
+        const ls_status r = launch_sequence(a, l, cfg, nullptr, nullptr, dt, key.ws, off, cs[key.dev], nl);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(cs[key.dev], &g);
+        cudaGraphExec_t x = nullptr;
+        const bool ok = r == LS_OK && ec == cudaSuccess && g &&
+                        cudaGraphInstantiate(&x, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {  // (not capturable here: keep running it directly, unless LS_GRAPH=2)
+            cudaGetLastError();
+            const char *gv = getenv("LS_GRAPH");
+            if (gv && gv[0] == '2') {
+                set_error("LS_GRAPH=2: capture of the launch sequence failed");
+                rc = LS_E_CUDA;
+                return true;
+            }
+            return false;
+        }
+        e->exec = x;
+        e->launches = nl;
+    }
+    const cudaError_t le = cudaGraphLaunch(e->exec, st);
+    if (le != cudaSuccess) {
+        rc = cuda_fail("cudaGraphLaunch", le);
+        return true;
+    }
+    launches = e->launches;
+    rc = LS_OK;
+    return true;
+}
+
+// Enqueue the whole sort. If `sync` the stream is synchronised and the status
+// and stats are collected; otherwise the caller synchronises (ls_sort_host).
+ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg_in,
+                       const ls_model *inject, void *d_ws, size_t ws_bytes, cudaStream_t st,
+                       ls_stats *stats, const ls_dumps *dumps, Pending *pend) {
+    ls_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    ls_status rc = check_config(cfg);
+    if (rc != LS_OK) return rc;
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    if (n >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    if (stats) memset(stats, 0, sizeof *stats);
+    if (stats) stats->n = n;
+    if (n <= 1) return LS_OK;
+    if (!d_keys || !d_ws) { set_error("null pointer"); return LS_E_INVALID; }
+    // the bulk-copy (TMA) stages and 16-byte vector loads address keys in aligned pairs
+    if (((uintptr_t)d_keys & 15) || ((uintptr_t)d_ws & 255)) {
+        set_error("keys must be 16-byte aligned and the workspace 256-byte aligned");
+        return LS_E_INVALID;
+    }
+    if (inject && !model_ok(*inject, cfg)) { set_error("injected model is not monotone-safe"); return LS_E_INVALID; }
+    const Layout l = make_layout(n, cfg);
+    if (ws_bytes < l.total) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    Args a = make_args(l, d_keys, d_ws);
+    if (const char *e = getenv("LS_DEBUG_STAGE")) a.dbg = (uint32_t)atoi(e);
+    // cluster-resident round 1 (SURVEY f2) with LS_FLAG_FUSED_ROUND1; LS_FR_MIN
+    // overrides the smallest bucket it takes (tests)
+    a.fr_cap = (cfg.flags & LS_FLAG_FUSED_ROUND1) ? round1_capacity() : 0u;
+    a.fr_min = a.fr_cap ? FR_MIN_DEFAULT : 0u;
+    if (const char *e = getenv("LS_FR_MIN")) a.fr_min = a.fr_cap ? (uint32_t)atoi(e) : 0u;
+    const int dt = (int)dtype;
+    if (dumps) {
+        a.dH0 = dumps->d_H0;
+        a.dH1 = dumps->d_H1;
+        if (a.dH0) LS_CUDA(cudaMemsetAsync(a.dH0, 0, (size_t)l.f, st));
+        if (a.dH1) LS_CUDA(cudaMemsetAsync(a.dH1, 0, (size_t)l.f * l.f, st));
+    }
+    Timer tm;
+    tm.start(cfg.flags & LS_FLAG_PHASE_TIMING, st);
+    uint64_t launches = 0;
+    bool done = false;
+    if (!inject && !dumps && !tm.on && !a.dbg && graphs_enabled()) {
+        GraphKey key;
+        memset(&key, 0, sizeof key);
+        key.keys = d_keys;
+        key.ws = d_ws;
+        key.n = n;
+        key.cfg = cfg;
+        key.dt = dt;
+        LS_CUDA(cudaGetDevice(&key.dev));
+        key.fr_min = a.fr_min;
+        key.dbg = a.dbg;
+        ls_status grc = LS_OK;
+        done = launch_graph(a, l, cfg, dt, key, st, launches, grc);
+        if (done && grc != LS_OK) return grc;
+    }
+    if (!done) {
+        const ls_status lrc = launch_sequence(a, l, cfg, inject, dumps, dt, d_ws, tm, st, launches);
+        if (lrc != LS_OK) return lrc;
+    }
     pend->ctl_dev = a.ctl;
     pend->model_dev = a.M;
     pend->launches = launches;

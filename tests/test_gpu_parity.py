@@ -508,3 +508,33 @@ def test_size_sweep_bit_exact(n):
         t = keys.clone()
         ls.ls_sort(t)
         assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
+
+
+# ------------------------------------------------ CUDA Graph replay (f2) --
+
+@pytest.mark.parametrize("n", [1_000_000, 3_000_001])
+def test_graph_replay_bit_exact(n, monkeypatch):
+    """the launch sequence is captured into a CUDA Graph the
+    second time the same (keys, n, dtype, config, workspace) comes back and
+    replayed afterwards. Different inputs through the same buffers must each
+    come out bit-exact (LS_GRAPH=2: a failed capture is an error, not a silent
+    direct launch); LS_GRAPH=0 (direct launches) gives the same bytes."""
+    monkeypatch.setenv("LS_GRAPH", "2")
+    t = torch.empty(n, dtype=torch.float64, device=DEV)
+    ws = ls.workspace(n, ls.LS_F64)
+    inputs = [("normal", 1), ("lognormal", 2), ("mixgauss", 3), ("normal", 4), ("uniform01", 5)]
+    for i, (dist, seed) in enumerate(inputs):
+        src = gen(dist, n, seed)
+        if i == 4:  # few distinct values and an all-equal run through the replayed graph
+            src[: n // 2] = 0.25
+        h = to_np(src)
+        t.copy_(src)
+        st = ls.ls_sort(t, ws=ws)
+        assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0])), (i, dist)
+        assert st["kernel_launches"] > 10
+        if i == 3:
+            monkeypatch.setenv("LS_GRAPH", "0")
+            t.copy_(src)
+            ls.ls_sort(t, ws=ws)
+            assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
+            monkeypatch.setenv("LS_GRAPH", "2")
