@@ -246,10 +246,18 @@ __device__ __forceinline__ int find_bucket(const uint32_t *ustart, int f, uint32
     return lo;
 }
 
+// Leaf staging of k_count1, measured per key type at 200M: fp64 keys run
+// faster with only the bucket's leaf range staged (static 2.5 KB; a wide range
+// reads the leaves through L1), uint64 keys (wide ranges over clustered
+// values) with every leaf in dynamic shared memory.
+template <int DT>
+constexpr bool C1_NARROW = DT == DT_F64;
+constexpr int C1_LEAVES = 64;
+
 template <int DT>
 __global__ void __launch_bounds__(512) k_count1(Args a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *leaf = reinterpret_cast<double *>(smem_raw);  // the model's leaves (5 L doubles)
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // (!C1_NARROW: all leaves)
+    __shared__ double s_leaf[C1_NARROW<DT> ? 5 * C1_LEAVES : 2];
     __shared__ uint32_t hist[LS_MAX_FANOUT];
     __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
     __shared__ unsigned long long s_mn[32], s_mx[32];
@@ -258,18 +266,41 @@ __global__ void __launch_bounds__(512) k_count1(Args a) {
     if (tid == 0) s_unit = atomicAdd(&a.ctl->ticket1, 1u);
     for (int b = tid; b <= f; b += bd) ustart[b] = a.unit1_start[b];
     for (int b = tid; b < f; b += bd) hist[b] = 0;
-    for (int i = tid; i < 5 * a.L; i += bd) leaf[i] = a.M->leaf[i];
     __syncthreads();
     const uint32_t u = s_unit;
     if (u >= a.ctl->U1 || a.ctl->status) return;
     const int b = find_bucket(ustart, f, u);
     if (a.fused[b]) return;  // partitioned by k_round1
+    // the leaves this bucket's keys can route to: the leaf index is monotone in
+    // the key, and the bucket holds the ords [thr[b-1], thr[b]) (b0 thresholds),
+    // so only leaves llo..lhi are staged (typically one or two, not all L)
+    const Root R = load_root(a.M);
+    const double *leaf = a.M->leaf;
+    {
+        double xc;
+        int llo = b > 0 ? root_leaf<DT>(from_ord<DT>(a.M->thr[b - 1]), R, xc) : 0;
+        int lhi = (uint32_t)b < a.M->nthr ? root_leaf<DT>(from_ord<DT>(a.M->thr[b] - 1ull), R, xc) : R.Lm1;
+        if (C1_NARROW<DT>) {
+            if (llo >= 0 && llo <= lhi && lhi - llo < C1_LEAVES) {
+                for (int i = tid; i < 5 * (lhi - llo + 1); i += bd) s_leaf[i] = a.M->leaf[5 * llo + i];
+                leaf = s_leaf - 5 * llo;
+            }  // (else through L1)
+        } else {
+            if (!(llo >= 0 && llo <= lhi && lhi <= R.Lm1)) {  // (defensive: stage them all)
+                llo = 0;
+                lhi = R.Lm1;
+            }
+            double *sl = reinterpret_cast<double *>(smem_raw);  // leaves at their own index
+            for (int i = 5 * llo + tid; i < 5 * (lhi + 1); i += bd) sl[i] = a.M->leaf[i];
+            leaf = sl;
+        }
+        __syncthreads();
+    }
     const uint32_t slice = u - ustart[b];
     const uint64_t bend = a.start0[b + 1];
     const uint64_t usz = unit1_size(a.start0[b], bend, ustart[b + 1] - ustart[b]);
     const uint64_t beg = umin64(bend, a.start0[b] + (uint64_t)slice * usz);  // (tile rounding can
     const uint64_t end = umin64(bend, beg + usz);                           //  leave a unit empty)
-    const Root R = load_root(a.M);
     unsigned long long mn = ~0ull, mx = 0;
     auto one = [&](uint64_t key) -> uint32_t {
         const unsigned long long o = to_ord<DT>(key);
@@ -559,7 +590,7 @@ void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
 }
 void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = (size_t)5 * a.L * sizeof(double);
-    if (dtype == DT_F64) { set_smem(k_count1<DT_F64>, sm); k_count1<DT_F64><<<a.U1max, 512, sm, st>>>(a); }
+    if (dtype == DT_F64) k_count1<DT_F64><<<a.U1max, 512, 0, st>>>(a);
     else { set_smem(k_count1<DT_U64>, sm); k_count1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
 }
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
