@@ -256,6 +256,7 @@ static bool model_ok(const ls_model &m, const ls_config &cfg) {
 
 struct Timer {
     bool on = false;
+    bool external = false;  // under stream capture: event-record nodes of the graph
     cudaEvent_t ev[LS_NUM_PHASES + 1];
     int phase_of[LS_NUM_PHASES + 1];
     int k = 0;
@@ -271,7 +272,8 @@ struct Timer {
     void mark(int phase) {
         if (!on) return;
         phase_of[k] = phase;
-        cudaEventRecord(ev[++k], st);
+        if (external) cudaEventRecordWithFlags(ev[++k], st, cudaEventRecordExternal);
+        else cudaEventRecord(ev[++k], st);
     }
     void finish(ls_stats *s) {
         if (!on) return;
@@ -352,8 +354,8 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
 // second time the same (keys, n, dtype, config, workspace, device) comes back
 // (one-shot calls run the sequence directly) and replayed with one
 // cudaGraphLaunch from then on. Off with LS_GRAPH=0; LS_GRAPH=2 turns a failed
-// capture into an error (tests). Never with an injected model (host sync),
-// dumps or phase timing.
+// capture into an error (tests). Never with an injected model (host sync) or
+// dumps; with LS_FLAG_PHASE_TIMING the phase events are graph nodes.
 struct GraphKey {
     void *keys, *ws;
     uint64_t n;
@@ -365,7 +367,19 @@ struct GraphEntry {
     GraphKey k;
     cudaGraphExec_t exec;  // null: seen once
     uint64_t launches, used;
+    // LS_FLAG_PHASE_TIMING: the phase events are recorded by the graph's own
+    // event-record nodes (owned here, read after each replay)
+    bool timed;
+    cudaEvent_t ev[LS_NUM_PHASES + 1];
+    int phase_of[LS_NUM_PHASES + 1];
+    int nmarks;
 };
+
+static void drop_graph(GraphEntry &g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);  // (freed after in-flight launches)
+    if (g.timed)
+        for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(g.ev[i]);
+}
 static std::mutex g_graph_mu;
 static std::vector<GraphEntry> g_graphs;
 static uint64_t g_graph_clock = 0;
@@ -383,7 +397,7 @@ static bool graphs_enabled() {
 
 // Run the sequence through the graph cache; false = not handled (run it directly).
 static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt, const GraphKey &key,
-                         cudaStream_t st, uint64_t &launches, ls_status &rc) {
+                         cudaStream_t st, uint64_t &launches, ls_status &rc, Pending *pend) {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     GraphEntry *e = nullptr;
     for (auto &g : g_graphs)
@@ -393,10 +407,14 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
             size_t lru = 0;
             for (size_t i = 1; i < g_graphs.size(); i++)
                 if (g_graphs[i].used < g_graphs[lru].used) lru = i;
-            if (g_graphs[lru].exec) cudaGraphExecDestroy(g_graphs[lru].exec);  // (freed after in-flight launches)
+            drop_graph(g_graphs[lru]);
             g_graphs.erase(g_graphs.begin() + lru);
         }
-        g_graphs.push_back(GraphEntry{key, nullptr, 0, ++g_graph_clock});
+        GraphEntry ne;
+        memset(&ne, 0, sizeof ne);
+        ne.k = key;
+        ne.used = ++g_graph_clock;
+        g_graphs.push_back(ne);
         return false;
     }
     e->used = ++g_graph_clock;
@@ -407,13 +425,25 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
             cudaGetLastError();
             return false;
         }
+        Timer cap;
+        cap.on = (cfg.flags & LS_FLAG_PHASE_TIMING) != 0;
+        cap.st = cs[key.dev];
+        cap.k = 0;
+        cap.external = true;
+        if (cap.on)
+            for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventCreate(&cap.ev[i]);
+        auto drop_events = [&] {
+            if (cap.on)
+                for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(cap.ev[i]);
+        };
         if (cudaStreamBeginCapture(cs[key.dev], cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
             cudaGetLastError();
+            drop_events();
             return false;
         }
-        Timer off;
+        if (cap.on) cudaEventRecordWithFlags(cap.ev[0], cs[key.dev], cudaEventRecordExternal);
         uint64_t nl = 0;
-        const ls_status r = launch_sequence(a, l, cfg, nullptr, nullptr, dt, key.ws, off, cs[key.dev], nl);
+        const ls_status r = launch_sequence(a, l, cfg, nullptr, nullptr, dt, key.ws, cap, cs[key.dev], nl);
         cudaGraph_t g = nullptr;
         const cudaError_t ec = cudaStreamEndCapture(cs[key.dev], &g);
         cudaGraphExec_t x = nullptr;
@@ -422,6 +452,7 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
         if (g) cudaGraphDestroy(g);
         if (!ok) {  // (not capturable here: keep running it directly, unless LS_GRAPH=2)
             cudaGetLastError();
+            drop_events();
             const char *gv = getenv("LS_GRAPH");
             if (gv && gv[0] == '2') {
                 set_error("LS_GRAPH=2: capture of the launch sequence failed");
@@ -432,6 +463,12 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
         }
         e->exec = x;
         e->launches = nl;
+        e->timed = cap.on;
+        if (cap.on) {
+            memcpy(e->ev, cap.ev, sizeof cap.ev);
+            memcpy(e->phase_of, cap.phase_of, sizeof cap.phase_of);
+            e->nmarks = cap.k;
+        }
     }
     const cudaError_t le = cudaGraphLaunch(e->exec, st);
     if (le != cudaSuccess) {
@@ -439,6 +476,13 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
         return true;
     }
     launches = e->launches;
+    pend->timer_on = e->timed;
+    pend->own_events = false;
+    if (e->timed) {
+        memcpy(pend->ev, e->ev, sizeof e->ev);
+        memcpy(pend->phase_of, e->phase_of, sizeof e->phase_of);
+        pend->nmarks = e->nmarks;
+    }
     rc = LS_OK;
     return true;
 }
@@ -480,11 +524,11 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         if (a.dH0) LS_CUDA(cudaMemsetAsync(a.dH0, 0, (size_t)l.f, st));
         if (a.dH1) LS_CUDA(cudaMemsetAsync(a.dH1, 0, (size_t)l.f * l.f, st));
     }
-    Timer tm;
-    tm.start(cfg.flags & LS_FLAG_PHASE_TIMING, st);
     uint64_t launches = 0;
     bool done = false;
-    if (!inject && !dumps && !tm.on && !a.dbg && graphs_enabled()) {
+    pend->timer_on = false;
+    pend->own_events = true;
+    if (!inject && !dumps && !a.dbg && graphs_enabled()) {
         GraphKey key;
         memset(&key, 0, sizeof key);
         key.keys = d_keys;
@@ -496,23 +540,25 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         key.fr_min = a.fr_min;
         key.dbg = a.dbg;
         ls_status grc = LS_OK;
-        done = launch_graph(a, l, cfg, dt, key, st, launches, grc);
+        done = launch_graph(a, l, cfg, dt, key, st, launches, grc, pend);
         if (done && grc != LS_OK) return grc;
     }
     if (!done) {
+        Timer tm;
+        tm.start(cfg.flags & LS_FLAG_PHASE_TIMING, st);
         const ls_status lrc = launch_sequence(a, l, cfg, inject, dumps, dt, d_ws, tm, st, launches);
         if (lrc != LS_OK) return lrc;
+        pend->timer_on = tm.on;
+        if (tm.on) {
+            memcpy(pend->ev, tm.ev, sizeof tm.ev);
+            memcpy(pend->phase_of, tm.phase_of, sizeof tm.phase_of);
+            pend->nmarks = tm.k;
+        }
     }
     pend->ctl_dev = a.ctl;
     pend->model_dev = a.M;
     pend->launches = launches;
     pend->dtype = dt;
-    pend->timer_on = tm.on;
-    if (tm.on) {
-        memcpy(pend->ev, tm.ev, sizeof tm.ev);
-        memcpy(pend->phase_of, tm.phase_of, sizeof tm.phase_of);
-        pend->nmarks = tm.k;
-    }
     LS_CUDA(cudaMemcpyAsync(&pend->ctl_host, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     if (dumps && dumps->h_model) {
         pend->model_host.reset(new DevModel);
@@ -549,7 +595,8 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
                 cudaEventElapsedTime(&ms, pend->ev[i], pend->ev[i + 1]);
                 stats->phase_ms[pend->phase_of[i]] += ms;
             }
-        for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(pend->ev[i]);
+        if (pend->own_events)
+            for (int i = 0; i <= LS_NUM_PHASES; i++) cudaEventDestroy(pend->ev[i]);
     }
     if (pend->model_out && pend->model_host) from_dev_model(*pend->model_host, pend->dtype, *pend->model_out);
     if (getenv("LS_DEBUG_STAGE")) {

@@ -20,6 +20,7 @@ struct Pending {
     uint64_t launches = 0;
     int dtype = 0;
     bool timer_on = false;
+    bool own_events = true;  // false: the events belong to a cached graph
     cudaEvent_t ev[LS_NUM_PHASES + 1];
     int phase_of[LS_NUM_PHASES + 1];
     int nmarks = 0;

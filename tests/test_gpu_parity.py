@@ -538,3 +538,23 @@ def test_graph_replay_bit_exact(n, monkeypatch):
             ls.ls_sort(t, ws=ws)
             assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
             monkeypatch.setenv("LS_GRAPH", "2")
+
+
+def test_graph_replay_phase_timing(monkeypatch):
+    """With LS_FLAG_PHASE_TIMING the phase events are event-record nodes of the
+    captured graph: the replayed sorts still report every phase's time."""
+    monkeypatch.setenv("LS_GRAPH", "2")
+    n = 2_000_000
+    t = torch.empty(n, dtype=torch.float64, device=DEV)
+    cfg = ls.config(flags=ls.LS_FLAG_PHASE_TIMING)
+    ws = ls.workspace(n, ls.LS_F64, cfg)
+    for seed in (1, 2, 3):
+        src = gen("normal", n, seed)
+        h = to_np(src)
+        t.copy_(src)
+        st = ls.ls_sort(t, cfg=cfg, ws=ws)
+        assert np.array_equal(bits(to_np(t)), bits(O.sort(h)[0]))
+        ph = st["phase_ms"]
+        for k in ("fit", "count0", "scatter0", "count1", "scatter1", "bucketsort"):
+            assert ph[k] > 0, (seed, k, ph)
+        assert sum(ph.values()) < 1000
