@@ -21,15 +21,20 @@ constexpr uint64_t LB_VALUE = (1ull << 62) - 1;
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 // --------------------------------------------------------------- keys ------
+// ord (IEEE totalOrder as an unsigned key): negative -> ~b, else b | 2^63.
+// Written as one xor with a sign mask (an arithmetic shift of the high word
+// and one 3-input logic op per word in SASS, no selects).
 template <int DT>
 __device__ __forceinline__ uint64_t to_ord(uint64_t b) {
     if (DT == DT_U64) return b;
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    const uint32_t hi = (uint32_t)(b >> 32), m = (uint32_t)((int32_t)hi >> 31);
+    return ((uint64_t)(hi ^ (m | 0x80000000u)) << 32) | (uint32_t)((uint32_t)b ^ m);
 }
 template <int DT>
 __device__ __forceinline__ uint64_t from_ord(uint64_t o) {
     if (DT == DT_U64) return o;
-    return (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+    const uint32_t hi = (uint32_t)(o >> 32), m = ~(uint32_t)((int32_t)hi >> 31);
+    return ((uint64_t)(hi ^ (m | 0x80000000u)) << 32) | (uint32_t)((uint32_t)o ^ m);
 }
 template <int DT>
 __device__ __forceinline__ double xd(uint64_t b) {
