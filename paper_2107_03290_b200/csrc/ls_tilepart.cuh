@@ -128,20 +128,25 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         }
         __syncthreads();
         mark(1);
-        // exclusive scan of the tile's bucket counts; advance the cursors
+        // every thread is past the previous tile's store phase: its ring slot
+        // is free for the tile after the next one
+        if (tid == 0 && i >= 1 && i - 1 + TP_NSLOT < ntl) {
+            const uint64_t tp0 = beg + (i - 1 + TP_NSLOT) * TP_TILE;
+            tp_issue(S, (int)((i - 1) % TP_NSLOT), src, tp0, umin64(end, tp0 + TP_TILE), len,
+                     BIDS ? bid : nullptr, sb);
+        }
+        // exclusive scan of the tile's bucket counts (bucket b <-> thread b):
+        // warp scans, then every warp adds the totals of the warps before it
+        // (one redux per warp instead of a second barrier-separated pass)
         uint32_t c = tid < nb ? S.cnt[tid] : 0u;
         const uint32_t incl = warp_incl_scan(c);
         if (lane == 31) S.wsum[warp] = incl;
         __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = S.wsum[lane];
-            const uint32_t vi = warp_incl_scan(v);
-            S.wsum[lane] = vi - v;
-            if (SKIP && lane == 31) S.tot = vi;  // keys that move in this tile
-        }
-        __syncthreads();
+        const uint32_t ws = S.wsum[lane];
+        const uint32_t wpre = __reduce_add_sync(0xffffffffu, lane < warp ? ws : 0u);
+        const uint32_t wtot = SKIP ? __reduce_add_sync(0xffffffffu, ws) : 0u;  // keys that move
         if (tid < nb) {
-            const uint32_t ex = S.wsum[warp] + incl - c;
+            const uint32_t ex = wpre + incl - c;
             S.ex[tid] = ex;
             S.delta[tid] = base[tid] - ex;
             base[tid] += c;
@@ -166,7 +171,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         __syncthreads();
         mark(3);
         {
-            const int tm = SKIP ? (int)S.tot : tn;
+            const int tm = SKIP ? (int)wtot : tn;
             uint32_t b[TP_KPT], d[TP_KPT];
             uint64_t v[TP_KPT];
 #pragma unroll
@@ -183,14 +188,12 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
                 if (idx < tm) dst[d[k] + (uint32_t)idx] = v[k];
             }
         }
-        __syncthreads();
+        // (no barrier: the next tile's first barrier orders these reads of the
+        // slot, sbin and delta before anything overwrites them)
         mark(4);
         phase ^= 1u << slot;
-        if (tid == 0 && i + TP_NSLOT < ntl)
-            tp_issue(S, slot, src, t0 + (uint64_t)TP_NSLOT * TP_TILE,
-                     umin64(end, t0 + (uint64_t)(TP_NSLOT + 1) * TP_TILE), len,
-                     BIDS ? bid : nullptr, sb);
     }
+    __syncthreads();  // (the caller may reuse the ring and tables right away)
 }
 
 __device__ __forceinline__ void tp_init(TpSmem &S) {
