@@ -89,7 +89,7 @@ struct Count0Smem {
 };
 
 template <int DT>
-__global__ void __launch_bounds__(512, 2) k_count0(Args a) {
+__global__ void __launch_bounds__(512, 3) k_count0(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Count0Smem &S = *reinterpret_cast<Count0Smem *>(smem_raw);
     uint32_t *hist = S.hist;
@@ -574,7 +574,7 @@ void launch_count0(const Args &a, int dtype, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned g = a.U0 < 2u * (uint32_t)sms ? a.U0 : 2u * (unsigned)sms;  // persistent, 2 per SM
+    const unsigned g = a.U0 < 3u * (uint32_t)sms ? a.U0 : 3u * (unsigned)sms;  // persistent, 3 per SM
     if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<g, 512, sm, st>>>(a); }
     else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<g, 512, sm, st>>>(a); }
 }
