@@ -255,7 +255,7 @@ constexpr bool C1_NARROW = DT == DT_F64;
 constexpr int C1_LEAVES = 64;
 
 template <int DT>
-__global__ void __launch_bounds__(512) k_count1(Args a) {
+__global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];  // (!C1_NARROW: all leaves)
     __shared__ double s_leaf[C1_NARROW<DT> ? 5 * C1_LEAVES : 2];
     __shared__ uint32_t hist[LS_MAX_FANOUT];
