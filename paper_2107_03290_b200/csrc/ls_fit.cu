@@ -17,13 +17,25 @@ __global__ void __launch_bounds__(256) k_sample_minmax(const uint64_t *__restric
                                                        uint64_t *__restrict__ S, Ctl *ctl) {
     unsigned long long mn = ~0ull, mx = 0;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gs) {
-        uint64_t b = src[k * stride];
-        if (S) S[k] = b;
-        if (is_finite_key<DT>(b) && !(DT == DT_F64 && is_nan_bits(b))) {
-            unsigned long long o = to_ord<DT>(b);
-            mn = o < mn ? o : mn;
-            mx = o > mx ? o : mx;
+    // strided gathers (one sector per key): 8 independent loads in flight per thread
+    constexpr int U = 8;
+    for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < m; k0 += U * gs) {
+        uint64_t b[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t k = k0 + u * gs;
+            b[u] = k < m ? __ldcs(src + k * stride) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t k = k0 + u * gs;
+            if (k >= m) continue;
+            if (S) S[k] = b[u];
+            if (is_finite_key<DT>(b[u]) && !(DT == DT_F64 && is_nan_bits(b[u]))) {
+                const unsigned long long o = to_ord<DT>(b[u]);
+                mn = o < mn ? o : mn;
+                mx = o > mx ? o : mx;
+            }
         }
     }
     mn = warp_min_u64(mn);
@@ -343,7 +355,7 @@ static int grid_for(uint64_t m, int block) {
 
 void launch_sample_minmax(const uint64_t *src, uint64_t stride, uint64_t m, uint64_t *S_out,
                           Ctl *ctl, int dtype, cudaStream_t st) {
-    int g = grid_for(m, 256);
+    int g = grid_for((m + 7) / 8, 256);
     if (dtype == DT_F64)
         k_sample_minmax<DT_F64><<<g, 256, 0, st>>>(src, stride, m, S_out, ctl);
     else
