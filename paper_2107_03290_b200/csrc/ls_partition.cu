@@ -392,17 +392,16 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
         for (uint64_t i = beg + tid; i < end; i += bd) a.A[i] = v;
         return;
     }
-    // sub-bucket starts of bucket b (exclusive scan of its S'_B row) + this unit's offsets
-    uint32_t *tst = S.tp.ex;
-    for (int j = tid; j < f; j += bd) tst[j] = a.hist1[(uint64_t)b * f + j];
+    // the first tiles are staged right away; meanwhile the cursors: sub-bucket
+    // starts (k_classify's start1) + this unit's offsets inside them
+    if (tid == 0) tp_issue_first(S.tp, a.B, beg, end, a.n, a.bid, &S.sbid);
+    for (int j = tid; j < f; j += bd)
+        S.base[j] = a.start1[(uint64_t)b * f + j] + a.offs1[(uint64_t)u * f + j];
     __syncthreads();
-    block_exscan(tst, f, S.tp.wsum);
-    for (int j = tid; j < f; j += bd) S.base[j] = (uint32_t)bbeg + tst[j] + a.offs1[(uint64_t)u * f + j];
-    tp_init(S.tp);
     uint32_t phase = 0;
     const NoBucket bf{};
-    tile_partition<false, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid,
-                                (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr);
+    tile_partition<false, true, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid,
+                                      (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr);
 }
 
 // ------------------------------------------------------------- classify ----

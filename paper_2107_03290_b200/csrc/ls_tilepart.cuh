@@ -79,7 +79,7 @@ __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *sr
 // by tp_init and every phase used so far is tracked in `phase`.
 // BIDS: the bucket of key i is bid[i] (precomputed by the count pass, staged
 // by the bulk engine next to the keys); bf is not called.
-template <bool SKIP = false, bool BIDS = false, class BF>
+template <bool SKIP = false, bool BIDS = false, bool ISSUED = false, class BF>
 __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
@@ -97,7 +97,7 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
     if (ntl == 0) return;
-    if (tid == 0)
+    if (!ISSUED && tid == 0)  // (ISSUED: the caller has staged the first tiles, tp_issue_first)
         for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && j < ntl; j++)
             tp_issue(S, (int)j, src, beg + j * TP_TILE, umin64(end, beg + (j + 1) * TP_TILE), len,
                      BIDS ? bid : nullptr, sb);
@@ -194,6 +194,18 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         phase ^= 1u << slot;
     }
     __syncthreads();  // (the caller may reuse the ring and tables right away)
+}
+
+// One thread: initialise the ring barriers and stage the first tiles of
+// [beg, end) at once (before the caller's own setup), for tile_partition<..,
+// ISSUED = true> after a block barrier.
+__device__ __forceinline__ void tp_issue_first(TpSmem &S, const uint64_t *src, uint64_t beg, uint64_t end,
+                                               uint64_t len, const uint16_t *bid = nullptr,
+                                               TpBids *sb = nullptr) {
+    for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.mbar[j], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (inits before the bulk copies)
+    for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && beg + j * TP_TILE < end; j++)
+        tp_issue(S, (int)j, src, beg + j * TP_TILE, umin64(end, beg + (j + 1) * TP_TILE), len, bid, sb);
 }
 
 __device__ __forceinline__ void tp_init(TpSmem &S) {
