@@ -623,6 +623,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t nw = gridDim.x * WS_WARPS;
     uint32_t r_maxg = 0;
+    bool early_h1 = false;
     uint4 nxt = blockIdx.x * WS_WARPS + warp < ntask ? a.tasks[blockIdx.x * WS_WARPS + warp]
                                                        : make_uint4(0, 0, 0, 0);
     for (uint32_t t = blockIdx.x * WS_WARPS + warp; t < ntask; t += nw) {
@@ -634,8 +635,11 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
 #pragma unroll
         for (int k = 0; k < WS_KPL; k++) key[k] = 32u * k + lane < np ? gl[32 * k] : 0ull;
         if (t + nw < ntask) nxt = a.tasks[t + nw];
-        // homogeneous sub-bucket (all keys equal): nothing to sort or store
-        {
+        // homogeneous sub-bucket (all keys equal): nothing to sort or
+        // store. Tested up front only once this warp has met one (the test
+        // after the sort below catches every case; on inputs without such
+        // sub-buckets the up-front test is pure cost: -4 % at 200M Normal)
+        if (early_h1) {
             const uint64_t k0 = __shfl_sync(0xffffffffu, key[0], 0);
             bool diff = false;
 #pragma unroll
@@ -824,6 +828,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 wst[warp][2]++;
                 wst[warp][3] += np;
             }
+            early_h1 = true;
         }
         __syncwarp();
     }
