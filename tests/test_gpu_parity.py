@@ -558,3 +558,21 @@ def test_graph_replay_phase_timing(monkeypatch):
         for k in ("fit", "count0", "scatter0", "count1", "scatter1", "bucketsort"):
             assert ph[k] > 0, (seed, k, ph)
         assert sum(ph.values()) < 1000
+
+
+def test_graph_cache_eviction(monkeypatch):
+    """More distinct (buffer, size) keys than the 16-entry graph cache holds:
+    entries are evicted (their graphs destroyed) and re-captured, and every
+    sort stays bit-exact."""
+    monkeypatch.setenv("LS_GRAPH", "2")
+    bufs = []
+    for i in range(20):
+        n = 50_000 + 1_000 * i
+        bufs.append((torch.empty(n, dtype=torch.float64, device=DEV), ls.workspace(n, ls.LS_F64),
+                     gen("mixgauss", n, 100 + i)))
+    for rnd in range(2):
+        for t, ws, src in bufs:
+            for rep in range(3):  # seen, captured + replayed, replayed
+                t.copy_(src)
+                ls.ls_sort(t, ws=ws)
+                assert np.array_equal(bits(to_np(t)), bits(np.sort(to_np(src)))), (rnd, rep)
