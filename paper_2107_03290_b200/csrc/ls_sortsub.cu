@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         // rounds as it has keys (2 rounds per iteration; none without
         // collisions; a clean pass ends it early on duplicate-heavy inputs).
         // Groups > 8 are sorted again by the warp bitonic below.
-        const int iters = (int)((mgs + 1u) >> 1);
+        const int iters = mgs > 1u ? (int)((mgs + 1u) >> 1) : 0;  // (no collision: nothing to do)
         if (iters > 0) {
             const uint32_t q0 = 8u * lane;
             uint64_t v[8];
