@@ -328,7 +328,7 @@ struct Args {
     unsigned long long *leaf_min;     // [L]
     unsigned long long *hist0;        // [f]
     unsigned long long *start0;       // [f+1]
-    unsigned long long *bmin0, *bmax0;// [f]
+    unsigned long long *bmin0, *bmax0;// [f] ord of bucket b's first key; != 0 iff two of its keys differ (H0)
     uint32_t *unit1_start;            // [f+1]
     unsigned long long *lb0;          // [U0*f]
     uint32_t *offs0;                  // [U0*f]

@@ -260,7 +260,6 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     __shared__ double s_leaf[C1_NARROW<DT> ? 5 * C1_LEAVES : 2];
     __shared__ uint32_t hist[LS_MAX_FANOUT];
     __shared__ uint32_t ustart[LS_MAX_FANOUT + 1];
-    __shared__ unsigned long long s_mn[32], s_mx[32];
     __shared__ uint32_t s_unit;
     const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
     if (tid == 0) s_unit = atomicAdd(&a.ctl->ticket1, 1u);
@@ -301,11 +300,11 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     const uint64_t usz = unit1_size(a.start0[b], bend, ustart[b + 1] - ustart[b]);
     const uint64_t beg = umin64(bend, a.start0[b] + (uint64_t)slice * usz);  // (tile rounding can
     const uint64_t end = umin64(bend, beg + usz);                           //  leave a unit empty)
-    unsigned long long mn = ~0ull, mx = 0;
+    // H0: is every key of bucket b equal to its first key?
+    const uint64_t k0 = a.B[a.start0[b]];
+    bool diff = false;
     auto one = [&](uint64_t key) -> uint32_t {
-        const unsigned long long o = to_ord<DT>(key);
-        mn = o < mn ? o : mn;
-        mx = o > mx ? o : mx;
+        diff |= key != k0;
         const double p = predict<DT>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
         const uint32_t b1 = bucket1(p, a.F2, f, (uint32_t)b);
         atomicAdd(&hist[b1], 1u);
@@ -336,21 +335,9 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
         }
         if (((end - i0) & 1) && tid == 0) a.bid[end - 1] = (uint16_t)one(a.B[end - 1]);
     }
-    mn = warp_min_u64(mn);
-    mx = warp_max_u64(mx);
-    if ((tid & 31) == 0) {
-        s_mn[tid >> 5] = mn;
-        s_mx[tid >> 5] = mx;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (int w = 1; w < (bd + 31) / 32; w++) {
-            mn = s_mn[w] < mn ? s_mn[w] : mn;
-            mx = s_mx[w] > mx ? s_mx[w] : mx;
-        }
-        atomicMin(&a.bmin0[b], mn);
-        atomicMax(&a.bmax0[b], mx);
-    }
+    // bmin0[b] = ord of the bucket's first key, bmax0[b] != 0 iff two keys differ
+    if (__syncthreads_or(diff) && tid == 0) a.bmax0[b] = 1ull;
+    if (tid == 0 && beg < end) a.bmin0[b] = to_ord<DT>(k0);
     for (int j = tid; j < f; j += bd) {
         const uint32_t c = hist[j];
         if (c) atomicAdd(&a.hist1[(uint64_t)b * f + j], c);
@@ -385,7 +372,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     const uint64_t beg = umin64(bend, bbeg + (uint64_t)slice * usz);  // (may be empty: tile rounding)
     const uint64_t end = umin64(bend, beg + usz);
     const unsigned long long mn = a.bmin0[b];
-    if (bend - bbeg <= 1 || mn == a.bmax0[b]) {
+    if (bend - bbeg <= 1 || a.bmax0[b] == 0ull) {
         // homogeneous level-0 bucket: already in final position
         // after defragmentation; here it is written straight from its value.
         const uint64_t v = from_ord<DT>(mn);
@@ -413,7 +400,7 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     const int b = blockIdx.x, f = a.f, tid = threadIdx.x;
     const uint64_t row = (uint64_t)b * f;
     const uint64_t bbeg = a.start0[b], nb = a.start0[b + 1] - bbeg;
-    const bool h0 = nb <= 1 || a.bmin0[b] == a.bmax0[b];
+    const bool h0 = nb <= 1 || a.bmax0[b] == 0ull;
     if (h0) {
         if (tid == 0) {
             if (a.dH0) a.dH0[b] = 1;

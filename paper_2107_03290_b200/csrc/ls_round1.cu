@@ -162,8 +162,8 @@ __global__ void __cluster_dims__(FR_CL, 1, 1) __launch_bounds__(FR_THREADS, 1) k
             gmx = m1 > gmx ? m1 : gmx;
         }
         if (rank == 0 && tid == 0) {
-            a.bmin0[b] = gmn;
-            a.bmax0[b] = gmx;
+            a.bmin0[b] = gmn;  // (k_count1's encoding: the value, and "two keys differ")
+            a.bmax0[b] = gmn != gmx ? 1ull : 0ull;
         }
         if (gmn == gmx) {
             // homogeneous level-0 bucket: final as its value
