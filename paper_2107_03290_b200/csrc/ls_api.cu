@@ -471,9 +471,11 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
         }
     }
     const cudaError_t le = cudaGraphLaunch(e->exec, st);
-    if (le != cudaSuccess) {
-        rc = cuda_fail("cudaGraphLaunch", le);
-        return true;
+    if (le != cudaSuccess) {  // (e.g. a stale graph after a context reset: forget it, launch directly)
+        cudaGetLastError();
+        drop_graph(*e);
+        g_graphs.erase(g_graphs.begin() + (e - g_graphs.data()));
+        return false;
     }
     launches = e->launches;
     pend->timer_on = e->timed;
