@@ -148,8 +148,10 @@ def predict(model: Model, keys: np.ndarray) -> np.ndarray:
 
 
 def sort(keys: np.ndarray, cfg: Config | None = None, model: Model | None = None,
-         dumps: bool = False):
-    """Run Alg. 2 on a copy. Returns (sorted, model, stats, dumps-dict|None)."""
+         dumps: bool | str = False):
+    """Run Alg. 2 on a copy. Returns (sorted, model, stats, dumps-dict|None).
+    dumps=True: every dump; dumps="tables": only the per-bucket tables (S_B,
+    S'_B, hist1_raw, H0, H1), no per-key arrays (full-size runs)."""
     a = keys.copy()
     u = _u64(a)
     n = len(u)
@@ -160,12 +162,14 @@ def sort(keys: np.ndarray, cfg: Config | None = None, model: Model | None = None
     dd = None
     dp = None
     if dumps:
-        dd = dict(p=np.zeros(n, np.float64), b0=np.zeros(n, np.uint32), b1=np.zeros(n, np.uint32),
-                  pos=np.zeros(n, np.uint32), S_B=np.zeros(f, np.uint64),
-                  S_B1=np.zeros(f * f, np.uint64), hist1_raw=np.zeros(f * f, np.uint64),
-                  H0=np.zeros(f, np.uint8), H1=np.zeros(f * f, np.uint8))
-        dp = Dumps(*[dd[k].ctypes.data for k in ("p", "b0", "b1", "pos", "S_B", "S_B1",
-                                                  "hist1_raw", "H0", "H1")])
+        dd = dict(S_B=np.zeros(f, np.uint64), S_B1=np.zeros(f * f, np.uint64),
+                  hist1_raw=np.zeros(f * f, np.uint64), H0=np.zeros(f, np.uint8),
+                  H1=np.zeros(f * f, np.uint8))
+        if dumps != "tables":
+            dd.update(p=np.zeros(n, np.float64), b0=np.zeros(n, np.uint32),
+                      b1=np.zeros(n, np.uint32), pos=np.zeros(n, np.uint32))
+        dp = Dumps(*[dd[k].ctypes.data if k in dd else None
+                     for k in ("p", "b0", "b1", "pos", "S_B", "S_B1", "hist1_raw", "H0", "H1")])
     rc = lib().lso_sort(u.ctypes.data, n, dtype_code(keys), C.byref(cfg),
                         C.byref(model) if model is not None else None, C.byref(mo),
                         C.byref(dp) if dp is not None else None, C.byref(st))

@@ -193,7 +193,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     return a;
 }
 
-static ls_status check_config(const ls_config &c) {
+ls_status check_config(const ls_config &c) {
     if (c.fanout < 2 || c.fanout > LS_MAX_FANOUT) { set_error("fanout out of range [2, 1024]"); return LS_E_INVALID; }
     if (c.leaf_count < 1 || c.leaf_count > LS_MAX_LEAVES) { set_error("leaf_count out of range [1, 1024]"); return LS_E_INVALID; }
     if (c.sample_stride < 1) { set_error("sample_stride must be >= 1"); return LS_E_INVALID; }
@@ -362,6 +362,7 @@ struct GraphKey {
     ls_config cfg;
     int dt, dev;
     uint32_t fr_min, dbg;
+    unsigned long long ctx;  // driver context id (cuCtxGetId): a graph never outlives its context
 };
 struct GraphEntry {
     GraphKey k;
@@ -387,12 +388,57 @@ constexpr size_t GRAPH_CACHE = 16;
 
 static bool same_key(const GraphKey &x, const GraphKey &y) {
     return x.keys == y.keys && x.ws == y.ws && x.n == y.n && x.dt == y.dt && x.dev == y.dev &&
-           x.fr_min == y.fr_min && x.dbg == y.dbg && !memcmp(&x.cfg, &y.cfg, sizeof x.cfg);
+           x.ctx == y.ctx && x.fr_min == y.fr_min && x.dbg == y.dbg && !memcmp(&x.cfg, &y.cfg, sizeof x.cfg);
 }
 
 static bool graphs_enabled() {
     const char *e = getenv("LS_GRAPH");
     return !(e && e[0] == '0');
+}
+
+// Id of the current driver context (unique per context, also across a
+// cudaDeviceReset that re-creates the primary context at the same address).
+// Resolved through the runtime's driver entry point, so libls does not link
+// libcuda. 0 = unknown (graphs are then not used).
+static unsigned long long current_ctx_id() {
+    typedef int (*GetCur)(void **);
+    typedef int (*GetId)(void *, unsigned long long *);
+    static GetCur get_cur = nullptr;
+    static GetId get_id = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuCtxGetCurrent", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_cur = (GetCur)f;
+        f = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuCtxGetId", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_id = (GetId)f;
+        cudaGetLastError();
+    });
+    void *ctx = nullptr;
+    unsigned long long id = 0;
+    if (!get_cur || !get_id || get_cur(&ctx) != 0 || !ctx || get_id(ctx, &id) != 0) return 0;
+    return id;
+}
+
+// Per-thread capture streams (one per device), recreated after a failed replay.
+static thread_local cudaStream_t g_cap_stream[64] = {};
+
+// Forget every cached graph and this thread's capture streams (after a replay
+// launch failed: handles from a destroyed context are not reused). Errors from
+// destroying stale handles are cleared afterwards.
+static void drop_all_graphs() {
+    for (auto &g : g_graphs) drop_graph(g);
+    g_graphs.clear();
+    for (auto &c : g_cap_stream)
+        if (c) {
+            cudaStreamDestroy(c);
+            c = nullptr;
+        }
+    cudaGetLastError();
 }
 
 // Run the sequence through the graph cache; false = not handled (run it directly).
@@ -419,7 +465,7 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
     }
     e->used = ++g_graph_clock;
     if (!e->exec) {  // second sight: capture on a private stream
-        static thread_local cudaStream_t cs[64] = {};
+        cudaStream_t *cs = g_cap_stream;
         if (key.dev < 0 || key.dev >= 64) return false;
         if (!cs[key.dev] && cudaStreamCreateWithFlags(&cs[key.dev], cudaStreamNonBlocking) != cudaSuccess) {
             cudaGetLastError();
@@ -470,11 +516,11 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
             e->nmarks = cap.k;
         }
     }
-    const cudaError_t le = cudaGraphLaunch(e->exec, st);
-    if (le != cudaSuccess) {  // (e.g. a stale graph after a context reset: forget it, launch directly)
-        cudaGetLastError();
-        drop_graph(*e);
-        g_graphs.erase(g_graphs.begin() + (e - g_graphs.data()));
+    cudaError_t le = cudaGraphLaunch(e->exec, st);
+    if (const char *f = getenv("LS_TEST_GRAPH_LAUNCH_FAIL"))  // (test hook: force the fallback below)
+        if (f[0] == '1') le = cudaErrorInvalidResourceHandle;
+    if (le != cudaSuccess) {  // a stale graph (e.g. after a context reset): forget every cached
+        drop_all_graphs();    // graph and capture stream, then launch the sequence directly
         return false;
     }
     launches = e->launches;
@@ -541,8 +587,9 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         LS_CUDA(cudaGetDevice(&key.dev));
         key.fr_min = a.fr_min;
         key.dbg = a.dbg;
+        key.ctx = current_ctx_id();
         ls_status grc = LS_OK;
-        done = launch_graph(a, l, cfg, dt, key, st, launches, grc, pend);
+        if (key.ctx) done = launch_graph(a, l, cfg, dt, key, st, launches, grc, pend);
         if (done && grc != LS_OK) return grc;
     }
     if (!done) {
@@ -684,7 +731,11 @@ ls_status ls_sort_with_model(void *d_keys, uint64_t n, ls_dtype dtype, const ls_
 
 ls_status ls_sort_host(void *h_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg, void *d_buf,
                        void *d_ws, size_t ws_bytes, void *stream, ls_stats *stats) {
-    if (n == 0) return LS_OK;
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        stats->n = n;
+    }
+    if (n <= 1) return LS_OK;  // (no copies: nothing is left in flight on return)
     if (!h_keys || !d_buf) { set_error("null pointer"); return LS_E_INVALID; }
     cudaStream_t st = (cudaStream_t)stream;
     LS_CUDA(cudaMemcpyAsync(d_buf, h_keys, n * 8, cudaMemcpyHostToDevice, st));

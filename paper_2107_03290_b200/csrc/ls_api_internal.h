@@ -27,6 +27,8 @@ struct Pending {
 };
 
 void set_error(const char *msg);
+// LS_OK or LS_E_INVALID (with ls_last_error set) for a bad ls_config.
+ls_status check_config(const ls_config &c);
 ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg,
                        const ls_model *inject, void *d_ws, size_t ws_bytes, cudaStream_t st,
                        ls_stats *stats, const ls_dumps *dumps, Pending *pend);

@@ -298,6 +298,7 @@ ls_status ls_multi_workspace_bytes(uint64_t n_in, uint64_t out_cap, int world, l
     ls_config cfg;
     if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
     if (!bytes || world < 1 || world > MAX_WORLD || (dtype != LS_F64 && dtype != LS_U64)) return LS_E_INVALID;
+    if (ls_status rc = check_config(cfg)) return rc;  // (before any layout arithmetic)
     *bytes = multi_layout(n_in, out_cap, world, cfg).total;
     return LS_OK;
 }
@@ -307,6 +308,7 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
                         void *d_ws, size_t ws_bytes, void *stream, ls_stats *stats) {
     ls_config cfg;
     if (cfg_in) cfg = *cfg_in; else ls_config_default(&cfg);
+    if (ls_status rc = check_config(cfg)) return rc;  // (before any layout work or collective)
     if (!comm || !n_out || !d_ws || (n_in && !d_in) || (out_cap && !d_out)) { set_error("null pointer"); return LS_E_INVALID; }
     if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
     if (n_in >= (1ull << 32) || out_cap >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }

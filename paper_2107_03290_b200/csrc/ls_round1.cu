@@ -34,6 +34,8 @@
 
 #include <type_traits>
 
+#include <mutex>
+
 #include "ls_common.cuh"
 #include "ls_launch.h"
 
@@ -230,11 +232,17 @@ __global__ void __cluster_dims__(FR_CL, 1, 1) __launch_bounds__(FR_THREADS, 1) k
     }
 }
 
-static int g_fr_clusters = -1;  // active clusters of k_round1 on this device (0: unavailable)
+// Active clusters of k_round1 per device (-1: not probed, 0: unavailable).
+// cudaFuncSetAttribute and the cluster occupancy are per device, so the probe
+// runs once per device (std::call_once per slot).
+constexpr int FR_MAX_DEV = 64;
+static int g_fr_clusters[FR_MAX_DEV];
+static std::once_flag g_fr_once[FR_MAX_DEV];
 
-uint32_t round1_capacity() {
-    if (g_fr_clusters < 0) {
-        g_fr_clusters = 0;
+static int fr_clusters(int dev) {
+    if (dev < 0 || dev >= FR_MAX_DEV) return 0;
+    std::call_once(g_fr_once[dev], [dev] {
+        g_fr_clusters[dev] = 0;
         const size_t sm = sizeof(FrSmem);
         if (cudaFuncSetAttribute(k_round1<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) ==
                 cudaSuccess &&
@@ -247,16 +255,29 @@ uint32_t round1_capacity() {
             c.dynamicSmemBytes = sm;
             int n = 0;
             if (cudaOccupancyMaxActiveClusters(&n, (void *)k_round1<DT_F64>, &c) == cudaSuccess && n > 0)
-                g_fr_clusters = n;
+                g_fr_clusters[dev] = n;
         }
         cudaGetLastError();  // clear a failed probe
+    });
+    return g_fr_clusters[dev];
+}
+
+static int current_device() {
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
     }
-    return g_fr_clusters > 0 ? (uint32_t)FR_CL * (FR_Q - 2) : 0u;  // (- 2: the staged slice's hull)
+    return d;
+}
+
+uint32_t round1_capacity() {
+    return fr_clusters(current_device()) > 0 ? (uint32_t)FR_CL * (FR_Q - 2) : 0u;  // (- 2: the staged slice's hull)
 }
 
 void launch_round1(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(FrSmem);
-    const dim3 grid((unsigned)(FR_CL * g_fr_clusters));
+    const dim3 grid((unsigned)(FR_CL * fr_clusters(current_device())));
     if (dtype == DT_F64) k_round1<DT_F64><<<grid, FR_THREADS, sm, st>>>(a);
     else k_round1<DT_U64><<<grid, FR_THREADS, sm, st>>>(a);
 }

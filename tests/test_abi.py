@@ -52,6 +52,20 @@ def test_host_only_entry_points():
     assert b"aligned" in ls.lib.ls_last_error()
     assert ls.lib.ls_sort(C.c_void_p(16), 100, 0, None, C.c_void_p(272), 1 << 40, None, None,
                           None) == ls.LS_E_INVALID
+    # ls_sort_host with n <= 1: returns before any copy is queued (nothing left
+    # in flight that could land in the caller's buffer after the call)
+    st.n = 99
+    assert ls.lib.ls_sort_host(C.c_void_p(8), 1, 0, None, None, None, 0, None, C.byref(st)) == ls.LS_OK
+    assert st.n == 1
+    # multi entry points validate the config before any layout arithmetic
+    # (sample_stride = 0 would divide by zero) or collective
+    z = ls.config()
+    z.sample_stride = 0
+    assert ls.lib.ls_multi_workspace_bytes(1000, 1000, 2, 0, C.byref(z), C.byref(out)) == ls.LS_E_INVALID
+    assert b"sample_stride" in ls.lib.ls_last_error()
+    n_out = C.c_uint64()
+    assert ls.lib.ls_sort_multi(None, None, 0, None, 0, C.byref(n_out), 0, C.byref(z), None, 0, None,
+                                None) == ls.LS_E_INVALID
     # structure sizes agree with the header (offsets of the trailing members)
     assert C.sizeof(ls.Model) == 4 + 4 + 8 + 4 + 4 + 3 * 8 + 1024 * 40
     assert C.sizeof(ls.Tagged) == 24

@@ -206,23 +206,33 @@ def test_spec_model_examples():
     assert O.predict(m, np.array([np.inf]))[0] == O.predict(m, np.array([s.max()]))[0]
 
 
-def test_sorted_input_bucket_counts():
-    """A[i] = i, n = 100·m, stride 100: the sample eCDF is exactly linear, so at
-    every sampled key below the last leaf p(100k) = 100k/n; an unsampled key sits
-    at most 99 keys below its leaf's first sample key (clamped to lo), so the
-    level-0 bucket b starts in [1000b - 99, 1000b]; b0 is monotone, sum S_B = n."""
-    n = 1_000_000
+@pytest.mark.parametrize("n", [1_000_000, 10_000_000])
+def test_sorted_input_bucket_counts(n):
+    """SURVEY §8(c) chord-leaf pin: A[i] = i, n = 100·m, stride 100. The sample
+    eCDF is exactly linear, so at every sampled key below the last leaf
+    p(100k) = 100k/n. Exact level-0 counts: bucket 999 = n/f + 99 (the 99 keys
+    above the last sample key clamp to PMAX), bucket 998 = n/f, buckets 0..997
+    hold n/f or n/f - 1 keys (a boundary key may round down one bucket), and
+    sum S_B = n (so exactly 99 of them hold n/f - 1); b0 is non-decreasing and
+    key i lies in bucket floor(i·f/n) or, when its p rounds up across the
+    boundary, the one above it."""
+    f = 1000
+    q = n // f
     a = np.arange(n, dtype=np.float64)
     m = O.train(a)
-    idx = np.arange(0, n - 1100, 100)
+    idx = np.arange(0, (n * 999) // 1000 - 100, 100)  # (below the last leaf)
     assert np.max(np.abs(O.predict(m, a[idx]) - idx / n)) < 1e-15
     _, _, _, d = O.sort(a, dumps=True)
     b0 = d["b0"].astype(np.int64)
     assert np.all(np.diff(b0) >= 0)
-    first = np.searchsorted(b0, np.arange(1000), side="left")
-    assert np.all(first[:999] <= 1000 * np.arange(999))
-    assert np.all(first[:999] >= 1000 * np.arange(999) - 99)
-    assert d["S_B"].sum() == n and np.array_equal(np.bincount(b0, minlength=1000), d["S_B"])
+    S = d["S_B"].astype(np.int64)
+    assert S.sum() == n and np.array_equal(np.bincount(b0, minlength=f), S)
+    assert S[999] == q + 99 and S[998] == q
+    assert set(np.unique(S[:998]).tolist()) <= {q - 1, q}
+    assert int(np.sum(S[:998] == q - 1)) == 99
+    i = np.arange((n * 998) // 1000, dtype=np.int64)
+    ideal = (i * f) // n
+    assert np.all((b0[i] == ideal) | (b0[i] == ideal + 1))
 
 
 # -------------------------------------------------------- ids / counting ----
@@ -338,6 +348,23 @@ def test_sort_equals_reference_1e6_and_invariants(dist):
     for b in range(f):
         seg = ou[starts[b]:starts[b + 1]]
         assert bool(d["H0"][b]) == (len(seg) <= 1 or bool(np.all(seg == seg[0])))
+    # H1 (Alg. 2, R11): for a bucket that is not homogeneous, sub-bucket
+    # (i, j) is flagged exactly when its range of the sorted output holds <= 1
+    # key or one value (sorted: first == last); rows of H0 buckets are zero
+    H1 = d["H1"].reshape(f, f).astype(bool)
+    assert not H1[rows].any()
+    sub_end = np.cumsum(raw).astype(np.int64)
+    sub_beg = sub_end - raw
+    nz = raw > 0
+    want = np.ones(f * f, bool)
+    first, last = ou[sub_beg[nz]], ou[sub_end[nz] - 1]
+    want[nz] = (raw[nz] <= 1) | (first == last)
+    want = want.reshape(f, f)
+    want[rows] = False
+    assert np.array_equal(H1, want)
+    assert int(H1.sum()) >= st["h1_subbuckets"]  # (stats count only sub-buckets of >= 2 keys)
+    hk = raw.reshape(f, f)[H1 & (raw.reshape(f, f) >= 2)]
+    assert st["h1_subbuckets"] == len(hk) and st["h1_keys"] == int(hk.sum())
     if dist == "rootdups":  # S:414 acceptance 7
         assert st["h1_subbuckets"] >= 1
 
