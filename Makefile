@@ -7,10 +7,13 @@ NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
 LS_SRC   := $(wildcard $(PKG)/csrc/*.cu)
 LS_HDR   := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/ls.h
 
-all: oracle/liboracle.so datagen/liblsgen.so $(PKG)/libls.so
+all: oracle/liboracle.so oracle/libhostsorts.so datagen/liblsgen.so $(PKG)/libls.so
 
 oracle/liboracle.so: oracle/ls2_oracle.c oracle/ls2_oracle.h
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -o $@ $< -lm
+
+oracle/libhostsorts.so: oracle/host_sorts.cpp
+	g++ -O2 -std=c++17 -fopenmp -fPIC -shared -Wall -o $@ $<
 
 datagen/liblsgen.so: datagen/lsgen.cu datagen/lsgen.h
 	$(NVCC) -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -shared -o $@ $<
@@ -23,6 +26,6 @@ $(PKG)/libls.so: $(patsubst $(PKG)/csrc/%.cu,$(PKG)/build/%.o,$(LS_SRC))
 	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib
 
 clean:
-	rm -rf $(PKG)/build $(PKG)/libls.so oracle/liboracle.so datagen/liblsgen.so
+	rm -rf $(PKG)/build $(PKG)/libls.so oracle/liboracle.so oracle/libhostsorts.so datagen/liblsgen.so
 
 .PHONY: all clean

@@ -135,8 +135,26 @@ def phase_bytes(phase: str, n: int, st: dict) -> float:
 
 
 def design_bytes(n: int, st: dict) -> float:
+    """The implementation's own per-phase bytes: count1 stores
+    each key's 2-byte b1, which scatter1 reads back (68 B/key on smooth inputs)."""
     return sum(phase_bytes(p, n, st) for p in ("fit", "count0", "scatter0", "count1", "scatter1",
                                                 "bucketsort", "big"))
+
+
+def class_bytes(n: int, st: dict) -> dict:
+    """SURVEY §8(d) algorithmic bytes per key class (8-byte keys), the
+    roofline numerator: U (key in a non-homogeneous level-0 bucket and a SMALL
+    sub-bucket) 56 = count0 r8 + round 0 r+w 16 + round 1 r+w 16 + in-bucket
+    sort r+w 16; H1 (homogeneous sub-bucket, also the single-key ones) 40;
+    H0 (homogeneous level-0 bucket) 24 = count0 8 + round-0 read 8 + fill
+    write 8; BIG 56 + 16 per MSD radix pass, counted here with one pass (72,
+    SURVEY App. A). Plus the fit's sample gather (one 32-B sector per sampled
+    key, < 1 B/key)."""
+    h0, h1, big, small = st["h0_keys"], st["h1_keys"], st["big_keys"], st["small_keys"]
+    single = max(0, n - h0 - h1 - big - small)
+    b = 56.0 * small + 40.0 * (h1 + single) + 24.0 * h0 + 72.0 * big + 32.0 * (n / 100.0)
+    return {"bytes": b, "bytes_per_key": b / n,
+            "keys": {"U": small, "H1": h1 + single, "H0": h0, "BIG": big}}
 
 
 def traffic_from_profiles(phase: str, n: int):
@@ -149,6 +167,118 @@ def traffic_from_profiles(phase: str, n: int):
     if not e or e.get("n") != n:
         return None
     return e.get("dram_bytes_per_launch")
+
+
+def _ord_signed(t):
+    """The total order of the keys (R12) as a signed int64 view (on device)."""
+    import torch
+    u = t.view(torch.int64)
+    if t.dtype == torch.float64:  # totalOrder: flip the magnitude bits of negatives
+        return torch.where(u < 0, u ^ torch.iinfo(torch.int64).max, u)
+    return u ^ torch.iinfo(torch.int64).min  # unsigned order as signed
+
+
+def is_sorted_dev(t) -> bool:
+    o = _ord_signed(t)
+    return bool((o[1:] >= o[:-1]).all().item())
+
+
+def dup_ratio_dev(t) -> float:
+    """1 - distinct/n of a sorted key array (SPEC's duplicate_ratio, bit equality)."""
+    import torch
+    u = t.view(torch.int64)
+    n = u.numel()
+    return 1.0 - (1 + int((u[1:] != u[:-1]).sum().item())) / n if n else 0.0
+
+
+def multiset_hash(t):
+    """(xor, sum) of splitmix64 over the 64-bit key patterns (order-free)."""
+    import torch
+    def c(x):
+        return x - (1 << 64) if x >= (1 << 63) else x
+
+    def lsr(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+    z = t.view(torch.int64) + c(0x9E3779B97F4A7C15)
+    z = (z ^ lsr(z, 30)) * c(0xBF58476D1CE4E5B9)
+    z = (z ^ lsr(z, 27)) * c(0x94D049BB133111EB)
+    z = z ^ lsr(z, 31)
+    total = int(z.sum().item())
+    while z.numel() > 1:
+        if z.numel() & 1:
+            z = torch.cat([z, z.new_zeros(1)])
+        z = z[0::2] ^ z[1::2]
+    return (int(z.item()) if z.numel() else 0, total)
+
+
+def ncu_step_traffic(n: int):
+    """Sum over the step's kernels of ncu dram bytes per launch (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    vals = [e.get("dram_bytes_per_launch") for e in d.values() if isinstance(e, dict) and e.get("n") == n]
+    return sum(v for v in vals if v) or None
+
+
+CONFIG_SET = ("c2_lognormal", "c2_exponential", "c2_mixgauss", "c3_zipf", "c3_rootdups", "c3_twodups",
+              "c4_telemetry", "ref_uniform01", "ref_uniform_u64")
+
+
+def time_configs(ls, keys, pristine, ws, cfg, stream, args, head) -> dict:
+    """BASELINE configs 2-4 (and the uniform references of the duplicate
+    budget) at 200M keys, on the bench's own buffers: 2 warm-up + `reps`
+    timed ls_sort calls each (median), sorted + multiset checked, dup ratio
+    and SURVEY §8(d) class bytes per config. Budget ratios = time / the
+    uniform time of the same key type (u64: ref_uniform_u64; f64:
+    ref_uniform01)."""
+    import numpy as np
+    import torch
+
+    import datagen
+    peak, _ = load_peaks()
+    n = keys.numel()
+    raw_p, raw_k = pristine.view(torch.int64), keys.view(torch.int64)
+    out = {}
+    reps = 5
+    for wl in CONFIG_SET:
+        dist_name, seed = datagen.WORKLOADS[wl]
+        plan = datagen.Plan(dist_name, n, seed)
+        tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
+        p_ = raw_p.view(tdt)
+        k_ = raw_k.view(tdt)
+        plan.device(p_)
+        torch.cuda.synchronize()
+        ms, st = [], None
+        for i in range(2 + reps):
+            k_.copy_(p_)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = ls.ls_sort(k_, cfg=cfg, ws=ws, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 2:
+                ms.append(e0.elapsed_time(e1))
+        med = statistics.median(ms)
+        cb = class_bytes(n, st)
+        out[wl] = {"dtype": "f64" if tdt == torch.float64 else "u64", "ms": med, "min_ms": min(ms),
+                   "keys_per_s": n / (med / 1e3), "dup_ratio": dup_ratio_dev(k_),
+                   "sorted_ok": is_sorted_dev(k_), "multiset_ok": multiset_hash(k_) == multiset_hash(p_),
+                   "bytes_per_key": cb["bytes_per_key"],
+                   "roofline_frac": cb["bytes"] / (med / 1e3) / 1e9 / peak,
+                   "phase_ms": {k: round(v, 4) for k, v in st["phase_ms"].items()},
+                   "class_keys": cb["keys"]}
+    out[head["config"]["workload"]] = {"dtype": head["dtype"], "ms": head["ms_per_step"],
+                                       "keys_per_s": head["value"], "dup_ratio": head["dup_ratio"]}
+    budget = {}
+    for wl, r in out.items():
+        ref = out.get("ref_uniform_u64" if r["dtype"] == "u64" else "ref_uniform01")
+        if ref and wl.startswith(("c3", "c4")):
+            budget[wl] = r["ms"] / ref["ms"]
+    return {"results": out, "dup_budget_vs_uniform": budget, "dup_budget_limit": 1.5,
+            "reps": reps, "note": "median of 5 timed ls_sort calls after 2 warm-ups, same buffers"}
 
 
 # ----------------------------------------------------------------- ours ----
@@ -247,14 +377,14 @@ def run_ours(args):
     step_ms = total_ms / args.steps
     dbytes = design_bytes(n_local, st0)
 
-    # correctness guard on the last step (cheap, on device): output non-decreasing
+    # correctness guard on the last step (on device): output non-decreasing and
+    # the same multiset as the input (xor and sum of a 64-bit mix of every key)
     res = (out[: n_out] if multi else keys)
-    u = res.view(torch.int64)
-    if res.dtype == torch.float64:  # totalOrder as a signed key: flip magnitude bits of negatives
-        o = torch.where(u < 0, u ^ torch.iinfo(torch.int64).max, u)
-    else:  # unsigned order as a signed key: flip the top bit
-        o = u ^ torch.iinfo(torch.int64).min
-    sorted_ok = bool((o[1:] >= o[:-1]).all().item())
+    sorted_ok = is_sorted_dev(res)
+    multiset_ok = None if multi else multiset_hash(res) == multiset_hash(pristine)
+    dup_ratio = None if multi else dup_ratio_dev(res)
+    cb = class_bytes(n_local, st0)
+    ncu_step = ncu_step_traffic(n_local)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -271,21 +401,34 @@ def run_ours(args):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profiles(dom, n_local),
                      "algorithmic_bytes_per_launch": b, "avg_launch_ms": phase_ms[dom],
                      "peak_source": peak_src},
-        "hbm_roofline_step": {"design_bytes": dbytes, "bytes_per_key": dbytes / n_local,
-                              "achieved_gbs": dbytes / (step_ms / 1e3) / 1e9,
-                              "frac": dbytes / (step_ms / 1e3) / 1e9 / peak,
-                              "frac_8tbs": dbytes / (step_ms / 1e3) / 1e9 / 8000.0},
+        # the whole step against SURVEY §8(d)'s roofline: class-weighted
+        # algorithmic bytes (56 / 40 / 24 / 72 B per key) / peak
+        "hbm_roofline_step": {"algorithmic_bytes": cb["bytes"], "bytes_per_key": cb["bytes_per_key"],
+                              "class_keys": cb["keys"],
+                              "achieved_gbs": cb["bytes"] / (step_ms / 1e3) / 1e9,
+                              "frac": cb["bytes"] / (step_ms / 1e3) / 1e9 / peak,
+                              "frac_8tbs": cb["bytes"] / (step_ms / 1e3) / 1e9 / 8000.0,
+                              "roofline_ms": cb["bytes"] / peak / 1e6,
+                              "impl_design_bytes_per_key": dbytes / n_local,
+                              "ncu_dram_bytes_per_key": (ncu_step / n_local) if ncu_step else None},
         "phase_ms": phase_ms,
         "class_keys": {k: st0[k] for k in ("h0_keys", "h1_keys", "small_keys", "big_keys",
                                            "big_subbuckets", "max_group")},
+        "dup_ratio": dup_ratio,
         "sorted_ok": sorted_ok,
+        "multiset_ok": multiset_ok,
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
         "clocks": clk.summary(),
     }
+    if not sorted_ok or multiset_ok is False:
+        line["value"] = None
+        line["error"] = "output check failed (sortedness or multiset hash)"
     if multi:
         line["n_out_rank0"] = n_out
 
-    # e2e: same metric through the C ABI with HOST buffers (ls_sort_host), copies timed
+    # e2e: the same metric through the C ABI with HOST buffers -- ls_sort_host:
+    # H2D of the pinned input, the sort, D2H of the sorted keys, all inside the
+    # timed region (one job at a time: PCIe-bound)
     if not multi and not args.no_e2e:
         host = torch.empty(n, dtype=tdt, pin_memory=True)
         host_pristine = pristine.cpu()
@@ -300,19 +443,23 @@ def run_ours(args):
             e1.synchronize()
             if i > 0:
                 e2e_ms.append(e0.elapsed_time(e1))
-        single = {"value": n / (statistics.mean(e2e_ms) / 1e3), "unit": UNIT,
-                  "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-                  "ms_per_step": statistics.mean(e2e_ms), "api": "ls_sort_host", "jobs_in_flight": 1}
-        line["e2e"] = single
-        if args.e2e_jobs > 1:
+        line["e2e"] = {"value": n / (statistics.mean(e2e_ms) / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                       "ms_per_step": statistics.mean(e2e_ms), "api": "ls_sort_host (C ABI, host buffers)",
+                       "jobs_in_flight": 1}
+        if args.e2e_jobs > 1:  # context: a service with several independent sorts in flight
             try:
-                line["e2e"] = e2e_pipelined(host_pristine, n, tdt, cfg, args.e2e_jobs,
-                                            max(2, min(args.steps, 4)))
-                line["e2e"]["single_job"] = single
-            except Exception as e:  # report the single-job number, say why
-                single["pipelined_unavailable"] = str(e)[:200]
+                line["e2e_pipelined"] = e2e_pipelined(host_pristine, n, tdt, cfg, args.e2e_jobs,
+                                                      max(2, min(args.steps, 4)))
+            except Exception as e:
+                line["e2e_pipelined"] = {"unavailable": str(e)[:200]}
         del host, host_pristine
 
+    # the other BASELINE configs (2-4) and the uniform references of the
+    # duplicate budget (north_star: high-duplicate inputs within 1.5x of
+    # uniform-input time), each timed the same way on the same buffers
+    if not multi and not args.no_configs and n == 200_000_000:
+        line["configs"] = time_configs(ls, keys, pristine, ws, cfg, stream, args, line)
     # e2e (multi-GPU): host shard -> device (pinned, H2D inside the timed region),
     # ls_sort_multi, this rank's sorted slice -> host; max over ranks
     if multi and not args.no_e2e:
@@ -348,7 +495,7 @@ def run_ours(args):
 
     # CPU baseline: the oracle as it stands, rank 0 at N=1, bounded sample
     if not multi and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(plan, args.cpu_sample)
+        line["cpu_baseline"] = cpu_baseline(plan, args.cpu_sample, args.std_sample)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -358,17 +505,50 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(plan, count: int) -> dict:
+def cpu_baseline(plan, count: int, std_count: int) -> dict:
+    """The oracle as it stands, single-threaded and pinned to one host core
+    (the paper's sequential setting), on a bounded prefix of the same
+    device-generated bytes; beside it, as context (SURVEY §8(d)), std::sort(≺)
+    on the same core and __gnu_parallel::sort(≺) on every core."""
     import oracle
     count = min(count, plan.n)
     h = plan_host_prefix(plan, count)
+    allowed = sorted(os.sched_getaffinity(0))
+    core = allowed[-1]
+    os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        oracle.sort(h)
+        dt = time.perf_counter() - t0
+        hs = h[: min(std_count, count)]
+        t0 = time.perf_counter()
+        oracle.std_sort(hs)
+        dts = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, set(allowed))
     t0 = time.perf_counter()
-    oracle.sort(h)
-    dt = time.perf_counter() - t0
+    _, threads = oracle.parallel_sort(h)
+    dtp = time.perf_counter() - t0
     return {"value": count / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"first {count} keys of the {plan.dist} workload (same device-generated "
                       f"bytes), oracle/ls2_oracle.c single-threaded, {dt:.1f} s",
-            "host_cpu": host_cpu()}
+            "pinned_core": core, "host_cpu": host_cpu(), "nproc": os.cpu_count(),
+            "lscpu": lscpu(),
+            "std_sort_1core": {"value": len(hs) / dts, "unit": UNIT, "cores": 1, "keys": len(hs),
+                               "s": dts},
+            "parallel_sort": {"value": count / dtp, "unit": UNIT, "cores": threads, "keys": count,
+                              "s": dtp, "impl": "__gnu_parallel::sort"}}
+
+
+def lscpu():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keep = ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)",
+                "CPU max MHz", "L3 cache")
+        return {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in out.splitlines() if ":" in ln)
+                if k.strip() in keep}
+    except Exception:
+        return None
 
 
 def plan_host_prefix(plan, count):
@@ -519,6 +699,10 @@ def main():
     ap.add_argument("--e2e-jobs", type=int, default=2,
                     help="independent sorts in flight for the e2e throughput (1: one at a time)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--std-sample", type=int, default=30_000_000,
+                    help="keys for the 1-core std::sort context baseline")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other 200M configs (dup budget) in the N=1 line")
     ap.add_argument("--force-multi", action="store_true",
                     help="run the ls_sort_multi path (config 5) even at world size 1")
     args = ap.parse_args()

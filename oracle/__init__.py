@@ -72,6 +72,44 @@ def build(force: bool = False) -> str:
 
 
 _lib = None
+_HS_SO = os.path.join(_HERE, "libhostsorts.so")
+_hs = None
+
+
+def build_host_sorts(force: bool = False) -> str:
+    """std::sort(≺) and __gnu_parallel::sort(≺) (oracle/host_sorts.cpp): the
+    CPU context baselines of bench.py's cpu_baseline leg."""
+    src = os.path.join(_HERE, "host_sorts.cpp")
+    if force or not os.path.exists(_HS_SO) or os.path.getmtime(_HS_SO) < os.path.getmtime(src):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-Wall",
+                               "-o", _HS_SO, src])
+    return _HS_SO
+
+
+def host_sorts():
+    global _hs
+    if _hs is None:
+        build_host_sorts()
+        L = C.CDLL(_HS_SO)
+        L.lso_std_sort.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+        L.lso_parallel_sort.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+        L.lso_parallel_sort.restype = C.c_int
+        _hs = L
+    return _hs
+
+
+def std_sort(keys: np.ndarray) -> np.ndarray:
+    """std::sort with the total-order comparator, on the calling thread."""
+    a = keys.copy()
+    host_sorts().lso_std_sort(_u64(a).ctypes.data, len(a), dtype_code(keys))
+    return a
+
+
+def parallel_sort(keys: np.ndarray):
+    """__gnu_parallel::sort with the same comparator; returns (sorted, threads)."""
+    a = keys.copy()
+    th = host_sorts().lso_parallel_sort(_u64(a).ctypes.data, len(a), dtype_code(keys))
+    return a, th
 
 
 def lib():

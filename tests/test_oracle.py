@@ -442,3 +442,20 @@ def test_edge_cases():
         r = np.sort(a)[::-1].copy()
         out, _, _, _ = O.sort(r)
         assert np.array_equal(out, np.sort(a))
+
+
+def test_host_sort_baselines_equal_reference():
+    """bench.py's CPU context baselines (oracle/host_sorts.cpp: std::sort(≺)
+    on one core, __gnu_parallel::sort(≺) on all cores) give the plain
+    definition of the result, including -0.0 before +0.0 and ±inf."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(200_000)
+    a[:6] = [-0.0, 0.0, np.inf, -np.inf, 5e-324, -5e-324]
+    rng.shuffle(a)
+    want = ref_sorted(a).view(np.uint64)
+    assert np.array_equal(O.std_sort(a).view(np.uint64), want)
+    p, threads = O.parallel_sort(a)
+    assert np.array_equal(p.view(np.uint64), want) and threads >= 1
+    u = rng.integers(0, 2 ** 64 - 1, 100_000, dtype=np.uint64)
+    assert np.array_equal(O.std_sort(u), np.sort(u))
+    assert np.array_equal(O.parallel_sort(u)[0], np.sort(u))
