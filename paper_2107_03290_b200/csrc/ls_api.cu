@@ -141,6 +141,10 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.F2 = (double)l.f * (double)l.f;
     a.nd = (double)l.n;
     a.rcpF2 = 1.0 / a.F2;
+    {
+        const double q = (double)l.n / a.F2;
+        a.S1 = q >= 1048576.0 ? 1048576u : (uint32_t)q + 2u;
+    }
     a.C0 = l.C0;
     a.C1 = l.C1;
     a.U0 = l.U0;

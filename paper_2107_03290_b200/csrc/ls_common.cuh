@@ -315,6 +315,7 @@ struct Args {
     int L;
     double F, F2, nd;
     double rcpF2;      // RN(1/f^2) for adj_of
+    uint32_t S1;       // ceil(n / f^2) + 1: slot range of the in-bucket counting sort (k_warpsort)
     uint32_t C0, C1;   // level-0 / level-1 unit sizes (keys)
     uint32_t U0, U1max;
     uint32_t T_small;  // big threshold

@@ -656,24 +656,68 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 continue;
             }
         }
-        for (uint32_t i = 4 * lane; i <= np; i += 128)
-            *reinterpret_cast<uint4 *>(&W.K[i]) = make_uint4(0, 0, 0, 0);
+        // Slots of the counting sort: pos = floor((p - adj) * n) (Alg. 2
+        // P:188-190) clamped to [0, S-1] with S = max(n', ceil(n/f^2) + 1)
+        // <= WS_MAX: R5 clamps to n'-1, which piles every key with pos >= n'-1
+        // of a sub-bucket smaller than n/f^2 into the last slot (one sorting
+        // network per such sub-bucket). The wider clamp refines R5's order (R5's
+        // pos = min(pos, n'-1), a monotone function of this one), so the
+        // placement is R5's counting sort with that top group already ordered
+        // by its unclamped positions; the touch-up finishes both identically.
+        const uint32_t S = max(np, min(a.S1, WS_MAX));
+        *reinterpret_cast<uint4 *>(&W.K[8 * lane]) = make_uint4(0, 0, 0, 0);  // K[0..256)
+        *reinterpret_cast<uint4 *>(&W.K[8 * lane + 4]) = make_uint4(0, 0, 0, 0);
         __syncwarp();
         // Alg. 2: pos per key (R5), K[pos]++ (the rank comes back).
         // Only the sub-buckets of xmin and xmax can hold keys outside
         // [xmin, xmax]; elsewhere the root clamp is skipped.
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
-        const int top = (int)(np - 1u);
+        const int top = (int)(S - 1u);
         uint32_t code[WS_KPL];
         if (g != g_lo && g != g_hi) {
+            // leaf of every key (O6 routing); a sub-bucket spans ~1/f^2 of the
+            // CDF, so its keys almost always share one leaf, whose line is then
+            // read once into registers instead of per key
+            int lf[WS_KPL];
+            int lmin = 1 << 30, lmax = -1;
 #pragma unroll
             for (int k = 0; k < WS_KPL; k++) {
-                code[k] = BS_NONE;
+                const double r = __dmul_rn(__dsub_rn(xd<DT>(key[k]), R.xmin), R.rs);
+                lf[k] = (r < R.last) ? __double2int_rz(r) : R.Lm1;
                 if (32u * k + lane < np) {
-                    const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
-                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
-                    const uint32_t r = atomicAdd(&W.K[pos], 1u);
-                    code[k] = pos | (r << 16);
+                    lmin = min(lmin, lf[k]);
+                    lmax = max(lmax, lf[k]);
+                }
+            }
+            lmin = __reduce_min_sync(0xffffffffu, lmin);
+            lmax = __reduce_max_sync(0xffffffffu, lmax);
+            if (lmin == lmax) {
+                const double *q = a.M->leaf + 5 * lmin;
+                const double la = __ldg(q), lc = __ldg(q + 1), lb = __ldg(q + 2), llo = __ldg(q + 3),
+                             lhi = __ldg(q + 4);
+#pragma unroll
+                for (int k = 0; k < WS_KPL; k++) {
+                    code[k] = BS_NONE;
+                    if (32u * k + lane < np) {
+                        const double y = __fma_rn(la, __dsub_rn(xd<DT>(key[k]), lc), lb);
+                        const double p = __dadd_rn(clampd(y, llo, lhi), 0.0);
+                        const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                        const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                        code[k] = pos | (r << 16);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < WS_KPL; k++) {
+                    code[k] = BS_NONE;
+                    if (32u * k + lane < np) {
+                        const double *q = a.M->leaf + 5 * lf[k];
+                        const double y = __fma_rn(__ldg(q), __dsub_rn(xd<DT>(key[k]), __ldg(q + 1)), __ldg(q + 2));
+                        const double p = __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
+                        const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                        const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                        code[k] = pos | (r << 16);
+                    }
                 }
             }
         } else {
@@ -689,42 +733,53 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             }
         }
         __syncwarp();
-        // exclusive running totals over np + 1 <= 257 entries, 9 per lane
-        uint32_t mgs = 0;  // largest collision group of <= BS_RANKMAX keys
+        // exclusive running totals over the S <= 256 slots, 8 per lane (two
+        // 16-byte loads / stores); K[S] = n' (for S < 256 the scan writes it)
+        uint32_t mgs;  // largest collision group of <= BS_RANKMAX keys
         {
-            constexpr int PER = 9;
-            uint32_t v[PER];
-            uint32_t sum = 0, bigm = 0;
+            const uint4 c0 = *reinterpret_cast<const uint4 *>(&W.K[8 * lane]);
+            const uint4 c1 = *reinterpret_cast<const uint4 *>(&W.K[8 * lane + 4]);
+            const uint32_t c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            uint32_t v[8], sum = 0, gmax = 0;
 #pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const uint32_t idx = PER * lane + q;
-                const uint32_t c = idx < np ? W.K[idx] : 0u;
-                mgs = (c <= BS_RANKMAX && c > mgs) ? c : mgs;
-                bigm |= (c > BS_RANKMAX ? 1u : 0u) << q;
+            for (int q = 0; q < 8; q++) {
                 v[q] = sum;
-                sum += c;
+                sum += c[q];
+                gmax = max(gmax, c[q]);
             }
             const uint32_t incl = warp_incl_scan(sum);
             const uint32_t off = incl - sum;
+            *reinterpret_cast<uint4 *>(&W.K[8 * lane]) = make_uint4(v[0] + off, v[1] + off, v[2] + off, v[3] + off);
+            *reinterpret_cast<uint4 *>(&W.K[8 * lane + 4]) = make_uint4(v[4] + off, v[5] + off, v[6] + off, v[7] + off);
+            gmax = __reduce_max_sync(0xffffffffu, gmax);
+            uint32_t nbl = 0;
+            if (gmax <= BS_RANKMAX) {
+                mgs = gmax;
+            } else {  // groups > 8 keys (duplicate-heavy inputs): list them (pos values)
+                uint32_t bigm = 0;
+                mgs = 0;
 #pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const uint32_t idx = PER * lane + q;
-                if (idx <= np) W.K[idx] = v[q] + off;
+                for (int q = 0; q < 8; q++) {
+                    mgs = (c[q] <= BS_RANKMAX && c[q] > mgs) ? c[q] : mgs;
+                    bigm |= (c[q] > BS_RANKMAX ? 1u : 0u) << q;
+                }
+                mgs = __reduce_max_sync(0xffffffffu, mgs);
+                const uint32_t nb = __popc(bigm);
+                const uint32_t pre = warp_incl_scan(nb) - nb;
+                uint32_t m = bigm, o = pre;
+                while (m) {
+                    const int q = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (o < 32) W.big[o] = 8 * lane + q;
+                    o++;
+                }
+                nbl = __shfl_sync(0xffffffffu, pre + nb, 31);  // total
             }
-            mgs = __reduce_max_sync(0xffffffffu, mgs);
             r_maxg = mgs > r_maxg ? mgs : r_maxg;  // (groups > 8: in the loop below)
-            // list the groups > 8 (pos values) for the warp sorts below
-            const uint32_t nbl = __popc(bigm);
-            const uint32_t pre = warp_incl_scan(nbl) - nbl;
-            uint32_t m = bigm, o = pre;
-            while (m) {
-                const int q = __ffs(m) - 1;
-                m &= m - 1;
-                if (o < 32) W.big[o] = PER * lane + q;
-                o++;
+            if (lane == 0) {
+                W.K[WS_MAX] = np;
+                W.K[WS_MAX + 7] = nbl;  // stash the count
             }
-            bigm = __shfl_sync(0xffffffffu, pre + nbl, 31);  // total
-            if (lane == 0) W.K[WS_MAX + 7] = bigm;  // stash the count
         }
         __syncwarp();
         // placement: T[K[pos] + r] = ord(key)
@@ -790,7 +845,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 } else {  // (more than 32 large groups: rescan the totals)
                     uint32_t seen = 0;
                     pos = 0;
-                    for (uint32_t x = 0; x < np; x++)
+                    for (uint32_t x = 0; x < S; x++)
                         if (W.K[x + 1] - W.K[x] > BS_RANKMAX && seen++ == k) { pos = x; break; }
                 }
                 const uint32_t base = W.K[pos], c = W.K[pos + 1] - base;
