@@ -678,15 +678,14 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
             // leaf of every key (O6 routing); a sub-bucket spans ~1/f^2 of the
             // CDF, so its keys almost always share one leaf, whose line is then
             // read once into registers instead of per key
-            int lf[WS_KPL];
             int lmin = 1 << 30, lmax = -1;
 #pragma unroll
             for (int k = 0; k < WS_KPL; k++) {
                 const double r = __dmul_rn(__dsub_rn(xd<DT>(key[k]), R.xmin), R.rs);
-                lf[k] = (r < R.last) ? __double2int_rz(r) : R.Lm1;
+                const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;
                 if (32u * k + lane < np) {
-                    lmin = min(lmin, lf[k]);
-                    lmax = max(lmax, lf[k]);
+                    lmin = min(lmin, l);
+                    lmax = max(lmax, l);
                 }
             }
             lmin = __reduce_min_sync(0xffffffffu, lmin);
@@ -711,9 +710,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 for (int k = 0; k < WS_KPL; k++) {
                     code[k] = BS_NONE;
                     if (32u * k + lane < np) {
-                        const double *q = a.M->leaf + 5 * lf[k];
-                        const double y = __fma_rn(__ldg(q), __dsub_rn(xd<DT>(key[k]), __ldg(q + 1)), __ldg(q + 2));
-                        const double p = __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
+                        const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
                         const uint32_t pos = cs_pos(p, adj, a.nd, top);
                         const uint32_t r = atomicAdd(&W.K[pos], 1u);
                         code[k] = pos | (r << 16);
@@ -775,7 +772,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 }
                 nbl = __shfl_sync(0xffffffffu, pre + nb, 31);  // total
             }
-            r_maxg = mgs > r_maxg ? mgs : r_maxg;  // (groups > 8: in the loop below)
+            r_maxg = gmax > r_maxg ? gmax : r_maxg;
             if (lane == 0) {
                 W.K[WS_MAX] = np;
                 W.K[WS_MAX + 7] = nbl;  // stash the count
@@ -800,7 +797,12 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         // collisions; a clean pass ends it early on duplicate-heavy inputs).
         // Groups > 8 are sorted again by the warp bitonic below.
         const int iters = mgs > 1u ? (int)((mgs + 1u) >> 1) : 0;  // (no collision: nothing to do)
-        if (iters > 0) {
+        const uint32_t nbl = W.K[WS_MAX + 7];
+        // A first pass that moves nothing has compared every adjacent pair:
+        // T is then sorted, groups > 8 included (duplicate-heavy inputs: equal
+        // keys share pos, so their large groups are runs of one value)
+        bool moved = false;
+        if (iters > 0 || nbl > 0) {
             const uint32_t q0 = 8u * lane;
             uint64_t v[8];
             {
@@ -824,20 +826,21 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                 if (lane > 0 && pv > v[0]) { v[0] = pv; moved = 1; }
                 return moved != 0;
             };
-            if (__any_sync(0xffffffffu, pass(true)))
+            moved = __any_sync(0xffffffffu, pass(true));
+            if (moved) {
                 for (int it2 = 1; it2 < iters; it2++) pass(false);
-            if (q0 < np) {
-                uint64_t *row = W.T + 9u * lane;
+                if (q0 < np) {
+                    uint64_t *row = W.T + 9u * lane;
 #pragma unroll
-                for (int q = 0; q < 8; q++) row[q] = v[q];
+                    for (int q = 0; q < 8; q++) row[q] = v[q];
+                }
             }
         }
         __syncwarp();
         // groups > 8 keys: register bitonic by the whole warp (the plain
         // select network: the single-predicate one costs the main path
         // registers here)
-        {
-            const uint32_t nbl = W.K[WS_MAX + 7];
+        if (moved) {
             for (uint32_t k = 0; k < nbl; k++) {
                 uint32_t pos;
                 if (nbl <= 32) {
@@ -849,7 +852,6 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
                         if (W.K[x + 1] - W.K[x] > BS_RANKMAX && seen++ == k) { pos = x; break; }
                 }
                 const uint32_t base = W.K[pos], c = W.K[pos + 1] - base;
-                r_maxg = c > r_maxg ? c : r_maxg;
                 bool same = true;
                 for (uint32_t q = lane; q < c; q += 32) same &= (T[base + q] == T[base]);
                 if (__all_sync(0xffffffffu, same)) continue;
