@@ -101,6 +101,8 @@ typedef struct {
     uint64_t big_passes;                /* radix passes spent on big sub-buckets              */
     uint64_t kernel_launches;           /* kernels this call launched                         */
     uint64_t fused_buckets;             /* level-0 buckets partitioned cluster-resident (f2)  */
+    uint64_t round0_exact;              /* 1: round 0 took the exact count pass (a sample-
+                                           estimated bucket capacity did not hold)           */
     float phase_ms[LS_NUM_PHASES];      /* with LS_FLAG_PHASE_TIMING                          */
 } ls_stats;
 
@@ -119,9 +121,11 @@ const char *ls_status_string(ls_status s);
 const char *ls_last_error(void);
 
 /* Device workspace needed by ls_sort / ls_sort_with_model / ls_train_rmi /
- * ls_bucket_ids for n keys (CUB-style size query). About 12n bytes + ~90 MB:
- * the scratch copy B of Alg. 2's partition rounds (8n), the round-1 bucket
- * ids (2n), the in-bucket task lists and big-item lists, per-unit tables. */
+ * ls_bucket_ids for n keys (CUB-style size query). About 14.7n bytes + ~90 MB:
+ * the scratch copy B of Alg. 2's partition rounds (n + n/4 + 4096 f keys:
+ * round 0 gives every level-0 bucket a sample-estimated region),
+ * the round-1 bucket ids (2 bytes per B slot), the in-bucket task and
+ * big-item lists, per-unit tables. */
 ls_status ls_workspace_bytes(uint64_t n, ls_dtype dtype, const ls_config *cfg, size_t *bytes);
 
 /* Fit F_A on a sample (north_star (1); R7-R9): d_sample holds m

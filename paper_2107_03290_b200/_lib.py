@@ -50,7 +50,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "n", "h0_buckets", "h0_keys", "h1_subbuckets", "h1_keys", "small_subbuckets",
         "small_keys", "big_subbuckets", "big_keys", "max_group", "big_passes",
-        "kernel_launches", "fused_buckets")] + [("phase_ms", C.c_float * len(PHASES))]
+        "kernel_launches", "fused_buckets", "round0_exact")] + [("phase_ms", C.c_float * len(PHASES))]
 
     def as_dict(self) -> dict:
         d = {n: int(getattr(self, n)) for n, _ in self._fields_[:-1]}

@@ -43,9 +43,11 @@ struct Layout {
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
+        cap0, bsrc, cur0, shist0,
         lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
+    uint64_t Bcap;
     size_t ff_begin, ff_end, zero_begin, zero_end, total;
 };
 
@@ -93,7 +95,11 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.tlast = take((size_t)l.ntiles * 4);
     l.ltot = take((size_t)l.lcap * 1024 * 4);
     l.lmax = take((size_t)l.lcap * 1024 * 8);
+    l.cur0 = take((size_t)l.f * 8);
+    l.shist0 = take((size_t)l.f * 4);
     l.zero_end = off;
+    l.cap0 = take((size_t)l.f * 8);
+    l.bsrc = take((size_t)(l.f + 1) * 8);
     l.ctl = take(sizeof(Ctl));
     l.model = take(sizeof(DevModel));
     l.S = take((size_t)l.m * 8);
@@ -103,7 +109,12 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
     l.wlist = take((size_t)l.ntiles * 16);
-    l.bid = take((size_t)(n + 16) * 2);
+    // B: the scratch copy of the partition rounds. Round 0 by reservation
+    // leaves each level-0 bucket a sample-estimated capacity (k_cap0), so B
+    // holds n + n/4 + 4096 f keys (more than the estimates in practice; when
+    // they do not fit, round 0 takes the exact count pass)
+    l.Bcap = n + n / 4 + (uint64_t)l.f * 4096;
+    l.bid = take((size_t)(l.Bcap + 16) * 2);
     l.task_cap = (uint32_t)((n / 2 + 1) < ff ? (n / 2 + 1) : ff);
     l.tasks = take((size_t)l.task_cap * 16);
     l.ctasks = take((size_t)l.task_cap * 16);
@@ -123,7 +134,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
     l.hist1_u64 = take(ff * 8);
-    l.B = take((size_t)n * 8);
+    l.B = take((size_t)l.Bcap * 8);
     l.total = align_up(off, 256);
     return l;
 }
@@ -172,6 +183,12 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.tile_last = (uint32_t *)(w + l.tlast);
     a.wlist = (uint4 *)(w + l.wlist);
     a.bid = (uint16_t *)(w + l.bid);
+    a.cap0 = (unsigned long long *)(w + l.cap0);
+    a.bsrc = (unsigned long long *)(w + l.bsrc);
+    a.cur0 = (unsigned long long *)(w + l.cur0);
+    a.shist0 = (uint32_t *)(w + l.shist0);
+    a.Bcap = l.Bcap;
+    a.force_exact0 = 0;
     a.tasks = (uint4 *)(w + l.tasks);
     a.ctasks = (uint4 *)(w + l.ctasks);
     a.ctasks2 = (uint4 *)(w + l.ctasks2);
@@ -317,14 +334,21 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     }
     launch_b0_table(a.M, l.L, l.f, dt, st);
     launches += 3;
-    tm.mark(LS_PHASE_FIT);
-    launch_count0(a, dt, st);
-    launch_plan0(a, dumps ? dumps->d_S_B : nullptr, st);
+    // round 0 by reservation: bucket capacities from the sample (k_cap0),
+    // then one scatter pass; the exact count pass (k_count0 + plan +
+    // k_scatter0) runs only when a capacity did not hold (kernels exit early)
+    launch_cap0(a, l.m, dt, st);
     launches += 2;
-    tm.mark(LS_PHASE_COUNT0);
-    launch_scatter0(a, dt, st);
-    launches++;
+    tm.mark(LS_PHASE_FIT);
+    launch_scatter0r(a, dt, st);
+    launch_plan0(a, dumps ? dumps->d_S_B : nullptr, 1, st);
+    launches += 2;
     tm.mark(LS_PHASE_SCATTER0);
+    launch_count0(a, dt, st);
+    launch_plan0(a, dumps ? dumps->d_S_B : nullptr, 0, st);
+    launch_scatter0(a, dt, st);
+    launches += 3;
+    tm.mark(LS_PHASE_COUNT0);
     if (a.fr_min) {  // buckets that fit a CTA cluster: count + scatter of round 1 in one kernel
         launch_round1(a, dt, st);
         launches++;
@@ -365,7 +389,7 @@ struct GraphKey {
     uint64_t n;
     ls_config cfg;
     int dt, dev;
-    uint32_t fr_min, dbg;
+    uint32_t fr_min, dbg, fx0;
     unsigned long long ctx;  // driver context id (cuCtxGetId): a graph never outlives its context
 };
 struct GraphEntry {
@@ -392,7 +416,7 @@ constexpr size_t GRAPH_CACHE = 16;
 
 static bool same_key(const GraphKey &x, const GraphKey &y) {
     return x.keys == y.keys && x.ws == y.ws && x.n == y.n && x.dt == y.dt && x.dev == y.dev &&
-           x.ctx == y.ctx && x.fr_min == y.fr_min && x.dbg == y.dbg && !memcmp(&x.cfg, &y.cfg, sizeof x.cfg);
+           x.ctx == y.ctx && x.fr_min == y.fr_min && x.dbg == y.dbg && x.fx0 == y.fx0 && !memcmp(&x.cfg, &y.cfg, sizeof x.cfg);
 }
 
 static bool graphs_enabled() {
@@ -568,6 +592,10 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
     // overrides the smallest bucket it takes (tests)
     a.fr_cap = (cfg.flags & LS_FLAG_FUSED_ROUND1) ? round1_capacity() : 0u;
     a.fr_min = a.fr_cap ? FR_MIN_DEFAULT : 0u;
+    // round 0 by the exact count pass: with the cluster-resident round 1 (it
+    // reads buckets at start0), or forced (LS_EXACT0=1, tests)
+    if (a.fr_cap) a.force_exact0 = 1;
+    if (const char *e = getenv("LS_EXACT0")) if (e[0] == '1') a.force_exact0 = 1;
     if (const char *e = getenv("LS_FR_MIN")) a.fr_min = a.fr_cap ? (uint32_t)atoi(e) : 0u;
     const int dt = (int)dtype;
     if (dumps) {
@@ -591,6 +619,7 @@ ls_status enqueue_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config
         LS_CUDA(cudaGetDevice(&key.dev));
         key.fr_min = a.fr_min;
         key.dbg = a.dbg;
+        key.fx0 = a.force_exact0;
         key.ctx = current_ctx_id();
         ls_status grc = LS_OK;
         if (key.ctx) done = launch_graph(a, l, cfg, dt, key, st, launches, grc, pend);
@@ -640,6 +669,7 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
         stats->big_passes = c.stat[ST_BIGPASS];
         stats->kernel_launches = pend->launches;
         stats->fused_buckets = c.nfused;
+        stats->round0_exact = c.exact0;
     }
     if (pend->timer_on) {
         if (stats)

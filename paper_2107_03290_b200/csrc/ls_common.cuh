@@ -288,6 +288,7 @@ struct Ctl {
     uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
     uint32_t nfill;                    // homogeneous pieces of large items (k_large_fill)
     uint32_t nfused, fticket;          // cluster-resident round 1: buckets listed / taken
+    uint32_t exact0;                   // 1: round 0 by the exact count pass (reservation declined or overflowed)
     unsigned long long smin, smax;     // finite sample ord min / max
     unsigned long long stat[ST_NUM];
     unsigned long long prof[16];       // debug cycle counters (LS_DEBUG_STAGE)
@@ -332,6 +333,12 @@ struct Args {
     unsigned long long *bmin0, *bmax0;// [f] ord of bucket b's first key; != 0 iff two of its keys differ (H0)
     uint32_t *unit1_start;            // [f+1]
     unsigned long long *lb0;          // [U0*f]
+    // round 0 by reservation (k_scatter0r): bucket b owns B[bsrc[b], bsrc[b] + cap0[b]),
+    // tiles reserve their runs with atomicAdd on cur0[b]; shist0 = sample counts
+    unsigned long long *cap0, *bsrc, *cur0;  // [f], [f+1], [f]
+    uint32_t *shist0;                 // [f]
+    uint64_t Bcap;                    // keys B holds (>= n)
+    uint32_t force_exact0;            // host: always take the exact count pass
     uint32_t *offs0;                  // [U0*f]
     uint32_t *offs1;                  // [U1max*f]
     uint32_t *hist1;                  // [f*f]

@@ -20,7 +20,9 @@ void launch_b0_table(DevModel *M, int L, int f, int dtype, cudaStream_t st);
 // partition rounds (ls_partition.cu)
 void launch_init(const Args &a, cudaStream_t st);
 void launch_count0(const Args &a, int dtype, cudaStream_t st);
-void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st);
+void launch_plan0(const Args &a, uint64_t *dS_B, int reserved, cudaStream_t st);
+void launch_cap0(const Args &a, uint64_t m, int dtype, cudaStream_t st);      // round 0 capacities
+void launch_scatter0r(const Args &a, int dtype, cudaStream_t st);             // round 0 by reservation
 void launch_scatter0(const Args &a, int dtype, cudaStream_t st);
 void launch_count1(const Args &a, int dtype, cudaStream_t st);
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st);

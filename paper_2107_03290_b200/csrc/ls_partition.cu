@@ -30,6 +30,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = 0;
         ctl->nfused = ctl->fticket = 0;
+        ctl->exact0 = 0;
         ctl->nlarge = ctl->npiece = 0;
         ctl->nfill = 0;
         for (int i = 0; i <= BIG_LEVELS; i++) ctl->big_cnt[i] = ctl->big_next[i] = 0;
@@ -90,6 +91,7 @@ struct Count0Smem {
 
 template <int DT>
 __global__ void __launch_bounds__(512, 3) k_count0(Args a) {
+    if (!a.ctl->exact0) return;  // (round 0 went by reservation, k_scatter0r)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Count0Smem &S = *reinterpret_cast<Count0Smem *>(smem_raw);
     uint32_t *hist = S.hist;
@@ -163,11 +165,27 @@ __device__ __forceinline__ uint64_t unit1_size(uint64_t bbeg, uint64_t bend, uin
 
 // S_B (Alg. 1 output), bucket starts (Alg. 2 read head) and the
 // round-1 unit plan. One block.
-__global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
+// reserved = 1: after k_scatter0r (runs only if the reservation held: no
+// bucket above its capacity; hist0 = the final cursors). reserved = 0: after
+// the exact count pass (runs only if round 0 had to be exact; bsrc = start0).
+__global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B, int reserved) {
     __shared__ uint32_t s[LS_MAX_FANOUT + 1];
     __shared__ uint32_t nu[LS_MAX_FANOUT + 1];
     __shared__ uint32_t tmp[33];
     const int f = a.f, tid = threadIdx.x;
+    if (reserved) {
+        if (a.ctl->exact0 || a.ctl->status) return;
+        bool over = false;
+        for (int b = tid; b < f; b += blockDim.x) over |= a.cur0[b] > a.cap0[b];
+        if (__syncthreads_or(over)) {
+            if (tid == 0) a.ctl->exact0 = 1u;
+            return;
+        }
+        for (int b = tid; b < f; b += blockDim.x) a.hist0[b] = a.cur0[b];
+        __syncthreads();
+    } else if (!a.ctl->exact0) {
+        return;
+    }
     for (int b = tid; b < f; b += blockDim.x) {
         const uint64_t h = a.hist0[b];
         s[b] = (uint32_t)h;
@@ -179,6 +197,7 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     const uint32_t units = block_exscan(nu, f, tmp);
     for (int b = tid; b < f; b += blockDim.x) {
         a.start0[b] = s[b];
+        if (!reserved) a.bsrc[b] = s[b];
         a.unit1_start[b] = nu[b];
         // cluster-resident round 1 (ls_round1.cu) for buckets of fr_min..fr_cap keys
         const uint64_t h = a.hist0[b];
@@ -188,6 +207,7 @@ __global__ void __launch_bounds__(1024) k_plan0(Args a, uint64_t *dS_B) {
     }
     if (tid == 0) {
         a.start0[f] = total;
+        if (!reserved) a.bsrc[f] = total;
         a.unit1_start[f] = units;
         a.ctl->U1 = units;
         if ((uint64_t)total != a.n) atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
@@ -216,7 +236,7 @@ struct Scatter0Smem {
 
 template <int DT>
 __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
-    if (a.ctl->status) return;
+    if (a.ctl->status || !a.ctl->exact0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Scatter0Smem &S = *reinterpret_cast<Scatter0Smem *>(smem_raw);
     const int f = a.f, tid = threadIdx.x;
@@ -232,8 +252,102 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
     tp_init(S.tp);
     const uint64_t beg = u0 * a.C0, end = umin64(a.n, u1 * a.C0);
     uint32_t phase = 0;
-    tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase, nullptr, nullptr,
+    tile_partition(S.tp, a.A, a.B, beg, end, a.n, S.base, f, bf, phase, nullptr, (TpBids *)nullptr,
                    (a.dbg & 1024u) ? a.ctl->prof : nullptr);
+}
+
+// ------------------------------------------- round 0 by reservation ------
+// The paper fills fixed-capacity fragments to avoid a separate counting scan
+// (P:263-267); here each level-0 bucket gets a capacity estimated from the 1 %
+// sample the model was fitted on (its sample count c_b, scaled by n/m, plus
+// 5 standard deviations), the scatter reserves every tile's run in its bucket
+// with one atomicAdd, and the count pass (k_count0) runs only if a bucket
+// overflowed or the capacities did not fit B. S_B = the final cursors (exact).
+template <int DT>
+__global__ void __launch_bounds__(256) k_samp_hist0(Args a, uint64_t m) {
+    __shared__ uint32_t h[LS_MAX_FANOUT];
+    const int f = a.f;
+    for (int b = threadIdx.x; b < f; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const DevModel *M = a.M;
+    const B0Search bs{M->xmin, M->xmax, M->cell_scale, M->nthr, M->thr, M->cell, M->sub};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[bs.get<DT>(a.S[i])], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < f; b += blockDim.x)
+        if (h[b]) atomicAdd(&a.shist0[b], h[b]);
+}
+
+__global__ void __launch_bounds__(1024) k_cap0(Args a, uint64_t m) {
+    __shared__ unsigned long long wsum[32];
+    const int f = a.f, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const double scale = (double)a.n / (double)(m ? m : 1);
+    unsigned long long cap = 0;
+    if (tid < f) {
+        const double c = (double)a.shist0[tid];
+        cap = (unsigned long long)ceil(scale * (c + 5.0 * sqrt(c) + 5.0));
+        a.cap0[tid] = cap;
+    }
+    // exclusive scan of the capacities (64-bit)
+    unsigned long long v = cap;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) wsum[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long x = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0ull, y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += t;
+        }
+        wsum[lane] = y - x;
+    }
+    __syncthreads();
+    const unsigned long long ex = wsum[w] + v - cap;
+    if (tid < f) a.bsrc[tid] = ex;
+    if (tid == f - 1) {
+        const unsigned long long total = ex + cap;
+        a.bsrc[f] = total;
+        if (a.force_exact0 || total > a.Bcap || a.Bcap + (uint64_t)TP_TILE >= (1ull << 32)) a.ctl->exact0 = 1u;
+    }
+}
+
+struct Scatter0rSmem {
+    TpSmem tp;
+    B0Smem b0;
+};
+
+template <int DT>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0r(Args a) {
+    if (a.ctl->status || a.ctl->exact0) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Scatter0rSmem &S = *reinterpret_cast<Scatter0rSmem *>(smem_raw);
+    __shared__ int s_nan;
+    // a contiguous run of tiles per CTA
+    const uint64_t ntiles = (a.n + TP_TILE - 1) / TP_TILE;
+    const uint64_t t0 = (uint64_t)blockIdx.x * ntiles / gridDim.x;
+    const uint64_t t1 = (uint64_t)(blockIdx.x + 1) * ntiles / gridDim.x;
+    if (t1 <= t0) return;
+    if (threadIdx.x == 0) s_nan = 0;
+    const B0Search bs = load_b0_search(S.b0, a.M);
+    tp_init(S.tp);
+    bool nan = false;
+    auto bf = [&](uint64_t key, uint64_t) -> uint32_t {
+        if (DT == DT_F64) nan |= is_nan_bits(key);
+        return bs.get<DT>(key);
+    };
+    const TpReserve rs{a.cur0, a.cap0, a.bsrc, &a.ctl->exact0, (uint32_t)a.Bcap};
+    uint32_t phase = 0;
+    tile_partition<false, false, false, decltype(bf), TP_THREADS, TP_KPT, TpBids, true>(
+        S.tp, a.A, a.B, t0 * TP_TILE, umin64(a.n, t1 * TP_TILE), a.n, nullptr, a.f, bf, phase, nullptr,
+        (TpBids *)nullptr, (a.dbg & 1024u) ? a.ctl->prof : nullptr, &rs);
+    if (nan) s_nan = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_nan) atomicOr(&a.ctl->status, (uint32_t)STATUS_NAN);
 }
 
 // --------------------------------------------------------------- round 1 ---
@@ -296,12 +410,13 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
         __syncthreads();
     }
     const uint32_t slice = u - ustart[b];
-    const uint64_t bend = a.start0[b + 1];
-    const uint64_t usz = unit1_size(a.start0[b], bend, ustart[b + 1] - ustart[b]);
-    const uint64_t beg = umin64(bend, a.start0[b] + (uint64_t)slice * usz);  // (tile rounding can
-    const uint64_t end = umin64(bend, beg + usz);                           //  leave a unit empty)
+    // bucket b sits in B at [bsrc[b], + its size) (round 0's reserved region)
+    const uint64_t bbeg = a.bsrc[b], bend = bbeg + (a.start0[b + 1] - a.start0[b]);
+    const uint64_t usz = unit1_size(bbeg, bend, ustart[b + 1] - ustart[b]);
+    const uint64_t beg = umin64(bend, bbeg + (uint64_t)slice * usz);  // (tile rounding can
+    const uint64_t end = umin64(bend, beg + usz);                    //  leave a unit empty)
     // H0: is every key of bucket b equal to its first key?
-    const uint64_t k0 = a.B[a.start0[b]];
+    const uint64_t k0 = a.B[bbeg];
     bool diff = false;
     auto one = [&](uint64_t key) -> uint32_t {
         diff |= key != k0;
@@ -353,6 +468,7 @@ struct Scatter1Smem {
 };
 
 static_assert(sizeof(Scatter0Smem) <= MAX_SMEM_OPTIN, "scatter0 shared memory");
+static_assert(sizeof(Scatter0rSmem) + 64 <= MAX_SMEM_OPTIN, "scatter0r shared memory");
 static_assert(sizeof(Scatter1Smem) <= MAX_SMEM_OPTIN, "scatter1 shared memory");
 
 template <int DT>
@@ -367,7 +483,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
     const int b = find_bucket(S.ustart, f, u);
     if (a.fused[b]) return;  // partitioned by k_round1
     const uint32_t slice = u - S.ustart[b];
-    const uint64_t bbeg = a.start0[b], bend = a.start0[b + 1];
+    // B side: the bucket's region from round 0 (bsrc); A side: start0
+    const uint64_t bbeg = a.bsrc[b], bend = bbeg + (a.start0[b + 1] - a.start0[b]);
     const uint64_t usz = unit1_size(bbeg, bend, S.ustart[b + 1] - S.ustart[b]);
     const uint64_t beg = umin64(bend, bbeg + (uint64_t)slice * usz);  // (may be empty: tile rounding)
     const uint64_t end = umin64(bend, beg + usz);
@@ -376,18 +493,19 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
         // homogeneous level-0 bucket: already in final position
         // after defragmentation; here it is written straight from its value.
         const uint64_t v = from_ord<DT>(mn);
-        for (uint64_t i = beg + tid; i < end; i += bd) a.A[i] = v;
+        uint64_t *Ab = a.A + a.start0[b] - bbeg;
+        for (uint64_t i = beg + tid; i < end; i += bd) Ab[i] = v;
         return;
     }
     // the first tiles are staged right away; meanwhile the cursors: sub-bucket
     // starts (k_classify's start1) + this unit's offsets inside them
-    if (tid == 0) tp_issue_first(S.tp, a.B, beg, end, a.n, a.bid, &S.sbid);
+    if (tid == 0) tp_issue_first(S.tp, a.B, beg, end, a.Bcap, a.bid, &S.sbid);
     for (int j = tid; j < f; j += bd)
         S.base[j] = a.start1[(uint64_t)b * f + j] + a.offs1[(uint64_t)u * f + j];
     __syncthreads();
     uint32_t phase = 0;
     const NoBucket bf{};
-    tile_partition<false, true, true>(S.tp, a.B, a.A, beg, end, a.n, S.base, f, bf, phase, a.bid, &S.sbid,
+    tile_partition<false, true, true>(S.tp, a.B, a.A, beg, end, a.Bcap, S.base, f, bf, phase, a.bid, &S.sbid,
                                       (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr);
 }
 
@@ -564,7 +682,25 @@ void launch_count0(const Args &a, int dtype, cudaStream_t st) {
     if (dtype == DT_F64) { set_smem(k_count0<DT_F64>, sm); k_count0<DT_F64><<<g, 512, sm, st>>>(a); }
     else { set_smem(k_count0<DT_U64>, sm); k_count0<DT_U64><<<g, 512, sm, st>>>(a); }
 }
-void launch_plan0(const Args &a, uint64_t *dS_B, cudaStream_t st) { k_plan0<<<1, 1024, 0, st>>>(a, dS_B); }
+void launch_plan0(const Args &a, uint64_t *dS_B, int reserved, cudaStream_t st) {
+    k_plan0<<<1, 1024, 0, st>>>(a, dS_B, reserved);
+}
+void launch_cap0(const Args &a, uint64_t m, int dtype, cudaStream_t st) {
+    const unsigned g = (unsigned)umin64((m + 1023) / 1024, 148);
+    if (dtype == DT_F64) k_samp_hist0<DT_F64><<<g ? g : 1, 256, 0, st>>>(a, m);
+    else k_samp_hist0<DT_U64><<<g ? g : 1, 256, 0, st>>>(a, m);
+    k_cap0<<<1, 1024, 0, st>>>(a, m);
+}
+void launch_scatter0r(const Args &a, int dtype, cudaStream_t st) {
+    const size_t sm = sizeof(Scatter0rSmem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t ntiles = (a.n + TP_TILE - 1) / TP_TILE;
+    const unsigned g = ntiles < (uint64_t)sms ? (unsigned)ntiles : (unsigned)sms;  // one CTA per SM
+    if (dtype == DT_F64) { set_smem(k_scatter0r<DT_F64>, sm); k_scatter0r<DT_F64><<<g, TP_THREADS, sm, st>>>(a); }
+    else { set_smem(k_scatter0r<DT_U64>, sm); k_scatter0r<DT_U64><<<g, TP_THREADS, sm, st>>>(a); }
+}
 void launch_scatter0(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(Scatter0Smem);
     int dev = 0, sms = 148;

@@ -27,20 +27,38 @@ constexpr int TP_THREADS = 1024;
 constexpr int TP_KPT = 8;
 constexpr int TP_TILE = TP_THREADS * TP_KPT;  // 8192 keys
 constexpr int TP_NSLOT = 2;                   // ring slots (3 slots of 6K-key tiles measured slower: shorter runs)
-constexpr int TP_SLOT = TP_TILE + 2;          // + aligned-hull slack
 
 constexpr size_t MAX_SMEM_OPTIN = 232448;  // 227 KB per block on sm_100
-typedef uint16_t TpBids[TP_NSLOT][TP_TILE + 16];  // staged precomputed bucket ids (BIDS mode)
 
-struct TpSmem {
-    uint64_t ring[TP_NSLOT][TP_SLOT];
-    uint16_t sbin[TP_TILE];
+// Shared memory of tile_partition for NT threads x KPT keys per tile.
+template <int NT, int KPT>
+struct TpSmemT {
+    static constexpr int TILE = NT * KPT;
+    static constexpr int SLOT = TILE + 2;  // + aligned-hull slack
+    uint64_t ring[TP_NSLOT][SLOT];
+    uint16_t sbin[TILE];
     uint32_t cnt[LS_MAX_FANOUT];
     uint32_t ex[LS_MAX_FANOUT];
     uint32_t delta[LS_MAX_FANOUT];
     uint32_t wsum[33];
     uint32_t tot;
     uint64_t mbar[TP_NSLOT];
+};
+typedef TpSmemT<TP_THREADS, TP_KPT> TpSmem;
+template <int TILE>
+using TpBidsT = uint16_t[TP_NSLOT][TILE + 16];  // staged precomputed bucket ids (BIDS mode)
+typedef TpBidsT<TP_TILE> TpBids;
+
+// Round 0 by reservation (k_scatter0r): instead of cursors from a count pass,
+// every tile reserves its run in bucket b with one atomicAdd on cur[b]; bucket
+// b owns dst[bsrc[b], bsrc[b] + cap[b]). A run that would pass cap[b] is not
+// written and raises *ovf (the caller then redoes the round exactly). lim =
+// an index no valid run reaches (stores at or beyond it are dropped).
+struct TpReserve {
+    unsigned long long *cur;
+    const unsigned long long *cap, *bsrc;
+    uint32_t *ovf;
+    uint32_t lim;
 };
 
 constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (SKIP mode)
@@ -50,9 +68,10 @@ constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (
 // copy covers the aligned hull [t0 & ~1, (t1 + 1) & ~1); only when that hull
 // would run past the end of the array (len odd, t1 == len) is the last key
 // loaded by this (single) thread directly.
-__device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *src, uint64_t t0,
+template <class SM, class SB = TpBids>
+__device__ __forceinline__ void tp_issue(SM &S, int slot, const uint64_t *src, uint64_t t0,
                                          uint64_t t1, uint64_t len, const uint16_t *bid = nullptr,
-                                         TpBids *sb = nullptr) {
+                                         SB *sb = nullptr) {
     uint64_t *dst = S.ring[slot];
     const uint64_t a0 = t0 & ~1ull;
     uint64_t a1 = (t1 + 1) & ~1ull;
@@ -79,13 +98,18 @@ __device__ __forceinline__ void tp_issue(TpSmem &S, int slot, const uint64_t *sr
 // by tp_init and every phase used so far is tracked in `phase`.
 // BIDS: the bucket of key i is bid[i] (precomputed by the count pass, staged
 // by the bulk engine next to the keys); bf is not called.
-template <bool SKIP = false, bool BIDS = false, bool ISSUED = false, class BF>
-__device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__restrict__ src,
+// RESERVE: base is unused; runs are reserved through *rs (TpReserve).
+template <bool SKIP = false, bool BIDS = false, bool ISSUED = false, class BF, int NT = TP_THREADS,
+          int KPT = TP_KPT, class SB = TpBids, bool RESERVE = false>
+__device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
                                                int nb, const BF &bf, uint32_t &phase,
-                                               const uint16_t *bid = nullptr, TpBids *sb = nullptr,
-                                               unsigned long long *prof = nullptr) {
+                                               const uint16_t *bid = nullptr, SB *sb = nullptr,
+                                               unsigned long long *prof = nullptr,
+                                               const TpReserve *rs = nullptr) {
+    constexpr int TILE = NT * KPT;
+    constexpr int BPT = (LS_MAX_FANOUT + NT - 1) / NT;  // buckets per thread in the scan
     long long tq = clock64();
     auto mark = [&](int k) {
         if (prof && threadIdx.x == 0) {
@@ -95,27 +119,27 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         }
     };
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t ntl = (end - beg + TP_TILE - 1) / TP_TILE;
+    const uint64_t ntl = (end - beg + TILE - 1) / TILE;
     if (ntl == 0) return;
     if (!ISSUED && tid == 0)  // (ISSUED: the caller has staged the first tiles, tp_issue_first)
         for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && j < ntl; j++)
-            tp_issue(S, (int)j, src, beg + j * TP_TILE, umin64(end, beg + (j + 1) * TP_TILE), len,
+            tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)j, src, beg + j * TILE, umin64(end, beg + (j + 1) * TILE), len,
                      BIDS ? bid : nullptr, sb);
-    if (tid < nb) S.cnt[tid] = 0;
+    for (int b = tid; b < nb; b += NT) S.cnt[b] = 0;
     __syncthreads();
     for (uint64_t i = 0; i < ntl; i++) {
         const int slot = (int)(i % TP_NSLOT);
-        const uint64_t t0 = beg + i * TP_TILE;
-        const int tn = (int)umin64((uint64_t)TP_TILE, end - t0);
+        const uint64_t t0 = beg + i * TILE;
+        const int tn = (int)umin64((uint64_t)TILE, end - t0);
         mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
         mark(0);
         const uint64_t *keys = S.ring[slot] + (t0 & 1);
         const uint16_t *bids = BIDS ? (*sb)[slot] + (t0 & 7) : nullptr;
-        uint64_t key[TP_KPT];
-        uint32_t code[TP_KPT];
+        uint64_t key[KPT];
+        uint32_t code[KPT];
 #pragma unroll
-        for (int k = 0; k < TP_KPT; k++) {
-            const int idx = k * TP_THREADS + tid;
+        for (int k = 0; k < KPT; k++) {
+            const int idx = k * NT + tid;
             code[k] = 0xffffffffu;
             if (idx < tn) {
                 key[k] = keys[idx];
@@ -131,61 +155,109 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
         // every thread is past the previous tile's store phase: its ring slot
         // is free for the tile after the next one
         if (tid == 0 && i >= 1 && i - 1 + TP_NSLOT < ntl) {
-            const uint64_t tp0 = beg + (i - 1 + TP_NSLOT) * TP_TILE;
-            tp_issue(S, (int)((i - 1) % TP_NSLOT), src, tp0, umin64(end, tp0 + TP_TILE), len,
+            const uint64_t tp0 = beg + (i - 1 + TP_NSLOT) * TILE;
+            tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)((i - 1) % TP_NSLOT), src, tp0, umin64(end, tp0 + TILE), len,
                      BIDS ? bid : nullptr, sb);
         }
-        // exclusive scan of the tile's bucket counts (bucket b <-> thread b):
-        // warp scans, then every warp adds the totals of the warps before it
-        // (one redux per warp instead of a second barrier-separated pass)
-        uint32_t c = tid < nb ? S.cnt[tid] : 0u;
+        // exclusive scan of the tile's bucket counts (buckets BPT*tid ..
+        // BPT*tid + BPT-1 <-> thread tid): warp scans, then every warp adds
+        // the totals of the warps before it (one redux per warp instead of a
+        // second barrier-separated pass)
+        uint32_t cb[BPT], c = 0;
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int b = BPT * tid + j;
+            cb[j] = b < nb ? S.cnt[b] : 0u;
+            c += cb[j];
+        }
+        // RESERVE: the runs are reserved now; the atomics' results are first
+        // needed after the placement below (their latency overlaps it)
+        unsigned long long rsv[RESERVE ? BPT : 1];
+        if (RESERVE) {
+#pragma unroll
+            for (int j = 0; j < BPT; j++) {
+                const int b = BPT * tid + j;
+                rsv[j] = cb[j] ? atomicAdd(&rs->cur[b], (unsigned long long)cb[j]) : 0ull;
+            }
+        }
         const uint32_t incl = warp_incl_scan(c);
         if (lane == 31) S.wsum[warp] = incl;
         __syncthreads();
-        const uint32_t ws = S.wsum[lane];
+        const uint32_t ws = lane < NT / 32 ? S.wsum[lane] : 0u;
         const uint32_t wpre = __reduce_add_sync(0xffffffffu, lane < warp ? ws : 0u);
         const uint32_t wtot = SKIP ? __reduce_add_sync(0xffffffffu, ws) : 0u;  // keys that move
-        if (tid < nb) {
-            const uint32_t ex = wpre + incl - c;
-            S.ex[tid] = ex;
-            S.delta[tid] = base[tid] - ex;
-            base[tid] += c;
-            S.cnt[tid] = 0;
+        const uint32_t ex0 = wpre + incl - c;
+        uint32_t ex = ex0;
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int b = BPT * tid + j;
+            if (b < nb) {
+                S.ex[b] = ex;
+                if (!RESERVE) {
+                    S.delta[b] = base[b] - ex;
+                    base[b] += cb[j];
+                }
+                S.cnt[b] = 0;
+            }
+            ex += cb[j];
         }
         __syncthreads();
         mark(2);
         // bucket-contiguous order inside the consumed slot (all lookups
         // first, then all stores: independent shared-memory chains)
         uint64_t *sk = S.ring[slot];
-        uint32_t pos[TP_KPT];
+        uint32_t pos[KPT];
 #pragma unroll
-        for (int k = 0; k < TP_KPT; k++)
+        for (int k = 0; k < KPT; k++)
             pos[k] = code[k] != 0xffffffffu ? S.ex[code[k] & 1023u] + (code[k] >> 10) : 0xffffffffu;
 #pragma unroll
-        for (int k = 0; k < TP_KPT; k++) {
+        for (int k = 0; k < KPT; k++) {
             if (pos[k] != 0xffffffffu) {
                 sk[pos[k]] = key[k];
                 S.sbin[pos[k]] = (uint16_t)(code[k] & 1023u);
+            }
+        }
+        if (RESERVE) {  // run starts from the reservations (delta = start - tile offset)
+            uint32_t e = ex0;
+#pragma unroll
+            for (int j = 0; j < BPT; j++) {
+                const int b = BPT * tid + j;
+                if (cb[j]) {
+                    uint32_t d;
+                    if (rsv[j] + cb[j] <= rs->cap[b]) {
+                        d = (uint32_t)(rs->bsrc[b] + rsv[j]) - e;
+                    } else {  // over capacity: dropped (the round is redone exactly)
+                        d = rs->lim;
+                        atomicOr(rs->ovf, 1u);
+                    }
+                    S.delta[b] = d;
+                }
+                e += cb[j];
             }
         }
         __syncthreads();
         mark(3);
         {
             const int tm = SKIP ? (int)wtot : tn;
-            uint32_t b[TP_KPT], d[TP_KPT];
-            uint64_t v[TP_KPT];
+            uint32_t b[KPT], d[KPT];
+            uint64_t v[KPT];
 #pragma unroll
-            for (int k = 0; k < TP_KPT; k++) {
-                const int idx = k * TP_THREADS + tid;
+            for (int k = 0; k < KPT; k++) {
+                const int idx = k * NT + tid;
                 b[k] = idx < tm ? S.sbin[idx] : 0u;
                 v[k] = sk[idx];
             }
 #pragma unroll
-            for (int k = 0; k < TP_KPT; k++) d[k] = S.delta[b[k]];
+            for (int k = 0; k < KPT; k++) d[k] = S.delta[b[k]];
 #pragma unroll
-            for (int k = 0; k < TP_KPT; k++) {
-                const int idx = k * TP_THREADS + tid;
-                if (idx < tm) dst[d[k] + (uint32_t)idx] = v[k];
+            for (int k = 0; k < KPT; k++) {
+                const int idx = k * NT + tid;
+                if (RESERVE) {
+                    const uint32_t q = d[k] + (uint32_t)idx;
+                    if (idx < tm && q < rs->lim) dst[q] = v[k];
+                } else if (idx < tm) {
+                    dst[d[k] + (uint32_t)idx] = v[k];
+                }
             }
         }
         // (no barrier: the next tile's first barrier orders these reads of the
@@ -199,16 +271,19 @@ __device__ __forceinline__ void tile_partition(TpSmem &S, const uint64_t *__rest
 // One thread: initialise the ring barriers and stage the first tiles of
 // [beg, end) at once (before the caller's own setup), for tile_partition<..,
 // ISSUED = true> after a block barrier.
-__device__ __forceinline__ void tp_issue_first(TpSmem &S, const uint64_t *src, uint64_t beg, uint64_t end,
-                                               uint64_t len, const uint16_t *bid = nullptr,
-                                               TpBids *sb = nullptr) {
+template <class SM, class SB = TpBids>
+__device__ __forceinline__ void tp_issue_first(SM &S, const uint64_t *src, uint64_t beg, uint64_t end,
+                                              uint64_t len, const uint16_t *bid = nullptr,
+                                              SB *sb = nullptr) {
+    constexpr int TILE = SM::TILE;
     for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.mbar[j], 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (inits before the bulk copies)
-    for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && beg + j * TP_TILE < end; j++)
-        tp_issue(S, (int)j, src, beg + j * TP_TILE, umin64(end, beg + (j + 1) * TP_TILE), len, bid, sb);
+    for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && beg + j * TILE < end; j++)
+        tp_issue<SM, SB>(S, (int)j, src, beg + j * TILE, umin64(end, beg + (j + 1) * TILE), len, bid, sb);
 }
 
-__device__ __forceinline__ void tp_init(TpSmem &S) {
+template <class SM>
+__device__ __forceinline__ void tp_init(SM &S) {
     if (threadIdx.x == 0)
         for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.mbar[j], 1);
     __syncthreads();

@@ -598,3 +598,25 @@ def test_graph_replay_launch_failure_falls_back(monkeypatch):
         t.copy_(src)
         ls.ls_sort(t, ws=ws)
         assert np.array_equal(bits(to_np(t)), bits(want)), i
+
+
+def test_round0_exact_fallback(monkeypatch):
+    """Round 0 by reservation (k_cap0 + k_scatter0r): bucket capacities come
+    from the 1 % strided sample. An input whose sample misrepresents it (every
+    100th key spread over [0, 1), the other 99 % inside [0, 0.001)) overflows
+    bucket 0's capacity; the call then takes the exact count pass (k_count0 +
+    k_scatter0) and is still bit-exact with the oracle, S_B / S'_B / H0 / H1
+    included. LS_EXACT0=1 forces the exact pass on a smooth input (same bytes
+    as the reservation path)."""
+    n = 1_000_000
+    rng = np.random.default_rng(9)
+    a = rng.random(n) * 1e-3
+    a[::100] = rng.random(len(a[::100]))
+    st, _ = check_sort(from_np(a))
+    assert st["round0_exact"] == 1
+    keys = gen("normal", 2_000_000, 4)
+    st, _ = check_sort(keys)
+    assert st["round0_exact"] == 0
+    monkeypatch.setenv("LS_EXACT0", "1")
+    st, _ = check_sort(keys)
+    assert st["round0_exact"] == 1
