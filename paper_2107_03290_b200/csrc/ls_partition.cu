@@ -337,7 +337,10 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0r(Args a) {
     tp_init(S.tp);
     bool nan = false;
     auto bf = [&](uint64_t key, uint64_t) -> uint32_t {
-        if (DT == DT_F64) nan |= is_nan_bits(key);
+        if (DT == DT_F64) {  // NaN check on the (otherwise idle) fp64 pipe: x != x
+            const double x = __longlong_as_double((long long)key);
+            nan |= x != x;
+        }
         return bs.get<DT>(key);
     };
     const TpReserve rs{a.cur0, a.cap0, a.bsrc, &a.ctl->exact0, (uint32_t)a.Bcap};

@@ -126,6 +126,16 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
             tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)j, src, beg + j * TILE, umin64(end, beg + (j + 1) * TILE), len,
                      BIDS ? bid : nullptr, sb);
     for (int b = tid; b < nb; b += NT) S.cnt[b] = 0;
+    // RESERVE: this thread's buckets' capacities and regions, once
+    unsigned long long rcap[RESERVE ? BPT : 1], rsrc[RESERVE ? BPT : 1];
+    if (RESERVE) {
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int b = BPT * tid + j;
+            rcap[j] = b < nb ? rs->cap[b] : 0ull;
+            rsrc[j] = b < nb ? rs->bsrc[b] : 0ull;
+        }
+    }
     __syncthreads();
     for (uint64_t i = 0; i < ntl; i++) {
         const int slot = (int)(i % TP_NSLOT);
@@ -224,8 +234,8 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
                 const int b = BPT * tid + j;
                 if (cb[j]) {
                     uint32_t d;
-                    if (rsv[j] + cb[j] <= rs->cap[b]) {
-                        d = (uint32_t)(rs->bsrc[b] + rsv[j]) - e;
+                    if (rsv[j] + cb[j] <= rcap[j]) {
+                        d = (uint32_t)(rsrc[j] + rsv[j]) - e;
                     } else {  // over capacity: dropped (the round is redone exactly)
                         d = rs->lim;
                         atomicOr(rs->ovf, 1u);
