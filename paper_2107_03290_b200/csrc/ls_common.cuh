@@ -126,6 +126,18 @@ __device__ __forceinline__ double predict(uint64_t bits, const Root &R, const do
     return __dadd_rn(clampd(y, q[3], q[4]), 0.0);
 }
 
+// predict() for keys known to lie in [xmin, xmax] when INNER (the root clamp
+// is the identity there); plain predict() otherwise.
+template <int DT, bool INNER>
+__device__ __forceinline__ double predict_c(uint64_t bits, const Root &R, const double *leaf) {
+    const double xc = INNER ? xd<DT>(bits) : clampd(xd<DT>(bits), R.xmin, R.xmax);
+    double r = __dmul_rn(__dsub_rn(xc, R.xmin), R.rs);
+    const int l = (r < R.last) ? __double2int_rz(r) : R.Lm1;
+    const double *q = leaf + 5 * l;
+    double y = __fma_rn(q[0], __dsub_rn(xc, q[1]), q[2]);
+    return __dadd_rn(clampd(y, q[3], q[4]), 0.0);
+}
+
 // Same, reading leaf parameters through the read-only path (keys of one
 // level-0 bucket share one or two leaves, so a warp's loads mostly broadcast).
 template <int DT>
@@ -152,15 +164,16 @@ __device__ __forceinline__ double predict_ldg_inner(uint64_t bits, const Root &R
 }
 
 // O7 / Alg.1 P:107 (R1)
+// (p in [0, 1) and f <= 1024, so p * f^2 < 2^20: a 32-bit truncation is the
+// same integer as the oracle's (int64) cast)
 __device__ __forceinline__ uint32_t bucket0(double p, double F, int f) {
-    long long b = __double2ll_rz(__dmul_rn(p, F));
-    return (uint32_t)(b < f - 1 ? b : f - 1);
+    const int b = __double2int_rz(__dmul_rn(p, F));
+    return (uint32_t)min(b, f - 1);
 }
 
 __device__ __forceinline__ uint32_t bucket1(double p, double F2, int f, uint32_t parent) {
-    long long b = __double2ll_rz(__dmul_rn(p, F2)) - (long long)parent * f;
-    b = b < 0 ? 0 : b;
-    return (uint32_t)(b > f - 1 ? f - 1 : b);
+    const int b = __double2int_rz(__dmul_rn(p, F2)) - (int)parent * f;
+    return (uint32_t)min(max(b, 0), f - 1);
 }
 
 // Sub-bucket of the prediction at the double xc (a root-clamped key).

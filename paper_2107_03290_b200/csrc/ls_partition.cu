@@ -370,6 +370,43 @@ __device__ __forceinline__ int find_bucket(const uint32_t *ustart, int f, uint32
 template <int DT>
 constexpr bool C1_NARROW = DT == DT_F64;
 constexpr int C1_LEAVES = 64;
+template <int DT, bool INNER>
+__device__ __forceinline__ void count1_range(const Args &a, int b, uint64_t beg, uint64_t end, uint64_t k0,
+                                             const Root &R, const double *leaf, uint32_t *hist, bool &diff) {
+    const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
+    auto one = [&](uint64_t key) -> uint32_t {
+        diff |= key != k0;
+        const double p = predict_c<DT, INNER>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
+        const uint32_t b1 = bucket1(p, a.F2, f, (uint32_t)b);
+        atomicAdd(&hist[b1], 1u);
+        return b1;
+    };
+    {
+        // 16-byte loads, 4 in flight per thread; odd head / tail keys apart.
+        // b1 of every key is kept (2 bytes) for k_scatter1.
+        uint64_t i0 = beg;
+        if ((i0 & 1) && i0 < end) {
+            if (tid == 0) a.bid[i0] = (uint16_t)one(a.B[i0]);
+            i0++;
+        }
+        const ulonglong2 *B2 = reinterpret_cast<const ulonglong2 *>(a.B + i0);
+        uint32_t *bid2 = reinterpret_cast<uint32_t *>(a.bid + i0);
+        const uint64_t np = (end - i0) / 2;
+        uint64_t i = tid;
+        for (; i + 3 * bd < np; i += 4 * bd) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = __ldcs(B2 + i + q * bd);
+#pragma unroll
+            for (int q = 0; q < 4; q++) bid2[i + q * bd] = one(v[q].x) | (one(v[q].y) << 16);
+        }
+        for (; i < np; i += bd) {
+            const ulonglong2 v = __ldcs(B2 + i);
+            bid2[i] = one(v.x) | (one(v.y) << 16);
+        }
+        if (((end - i0) & 1) && tid == 0) a.bid[end - 1] = (uint16_t)one(a.B[end - 1]);
+    }
+}
 
 template <int DT>
 __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
@@ -421,38 +458,14 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     // H0: is every key of bucket b equal to its first key?
     const uint64_t k0 = a.B[bbeg];
     bool diff = false;
-    auto one = [&](uint64_t key) -> uint32_t {
-        diff |= key != k0;
-        const double p = predict<DT>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
-        const uint32_t b1 = bucket1(p, a.F2, f, (uint32_t)b);
-        atomicAdd(&hist[b1], 1u);
-        return b1;
-    };
-    {
-        // 16-byte loads, 4 in flight per thread; odd head / tail keys apart.
-        // b1 of every key is kept (2 bytes) for k_scatter1.
-        uint64_t i0 = beg;
-        if ((i0 & 1) && i0 < end) {
-            if (tid == 0) a.bid[i0] = (uint16_t)one(a.B[i0]);
-            i0++;
-        }
-        const ulonglong2 *B2 = reinterpret_cast<const ulonglong2 *>(a.B + i0);
-        uint32_t *bid2 = reinterpret_cast<uint32_t *>(a.bid + i0);
-        const uint64_t np = (end - i0) / 2;
-        uint64_t i = tid;
-        for (; i + 3 * bd < np; i += 4 * bd) {
-            ulonglong2 v[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) v[q] = __ldcs(B2 + i + q * bd);
-#pragma unroll
-            for (int q = 0; q < 4; q++) bid2[i + q * bd] = one(v[q].x) | (one(v[q].y) << 16);
-        }
-        for (; i < np; i += bd) {
-            const ulonglong2 v = __ldcs(B2 + i);
-            bid2[i] = one(v.x) | (one(v.y) << 16);
-        }
-        if (((end - i0) & 1) && tid == 0) a.bid[end - 1] = (uint16_t)one(a.B[end - 1]);
-    }
+    // only the buckets of xmin and xmax can hold keys outside [xmin, xmax]
+    // (they are clamped onto xmin / xmax): elsewhere the root clamp is skipped
+    const uint32_t b_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, f) / (uint32_t)f;
+    const uint32_t b_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, f) / (uint32_t)f;
+    if ((uint32_t)b != b_lo && (uint32_t)b != b_hi)
+        count1_range<DT, true>(a, b, beg, end, k0, R, leaf, hist, diff);
+    else
+        count1_range<DT, false>(a, b, beg, end, k0, R, leaf, hist, diff);
     // bmin0[b] = ord of the bucket's first key, bmax0[b] != 0 iff two keys differ
     if (__syncthreads_or(diff) && tid == 0) a.bmax0[b] = 1ull;
     if (tid == 0 && beg < end) a.bmin0[b] = to_ord<DT>(k0);
