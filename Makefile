@@ -9,8 +9,8 @@ LS_HDR   := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/ls
 
 all: oracle/liboracle.so oracle/libhostsorts.so datagen/liblsgen.so $(PKG)/libls.so
 
-oracle/liboracle.so: oracle/ls2_oracle.c oracle/ls2_oracle.h
-	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -o $@ $< -lm
+oracle/liboracle.so: oracle/ls2_oracle.c oracle/ls1_oracle.c oracle/ls2_oracle.h
+	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -Wall -o $@ oracle/ls2_oracle.c oracle/ls1_oracle.c -lm
 
 oracle/libhostsorts.so: oracle/host_sorts.cpp
 	g++ -O2 -std=c++17 -fopenmp -fPIC -shared -Wall -o $@ $<

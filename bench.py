@@ -524,6 +524,7 @@ def cpu_baseline(plan, count: int, std_count: int) -> dict:
         t0 = time.perf_counter()
         oracle.std_sort(hs)
         dts = time.perf_counter() - t0
+        ls1 = ls1_context(oracle, h[:LS1_KEYS], plan.dist)
     finally:
         os.sched_setaffinity(0, set(allowed))
     t0 = time.perf_counter()
@@ -537,7 +538,32 @@ def cpu_baseline(plan, count: int, std_count: int) -> dict:
             "std_sort_1core": {"value": len(hs) / dts, "unit": UNIT, "cores": 1, "keys": len(hs),
                                "s": dts},
             "parallel_sort": {"value": count / dtp, "unit": UNIT, "cores": threads, "keys": count,
-                              "s": dtp, "impl": "__gnu_parallel::sort"}}
+                              "s": dtp, "impl": "__gnu_parallel::sort"},
+            "ls1_vs_ls2": ls1}
+
+
+LS1_KEYS = 10_000_000
+
+
+def ls1_context(oracle, head, dist):
+    """the LearnedSort 1.0 oracle variant (spill bucket +
+    exception table, oracle/ls1_oracle.c) against the LS 2.0 oracle on the
+    same core and the same keys -- the host-side counterpart of the paper's
+    LS 2.0 / LS 1.0 ratios (1.60x low-duplicate, >= 1.6x TwoDups, 4.78x
+    high-duplicate average: P:27). Context only."""
+    import datagen
+    out = {"keys": LS1_KEYS, "paper": {"low_dup": 1.60, "twodups_min": 1.6, "high_dup_avg": 4.78}}
+    for name, keys in ((dist, head), ("twodups", datagen.generate_host("twodups", LS1_KEYS, 1)),
+                       ("zipf", datagen.generate_host("zipf", LS1_KEYS, 1))):
+        t0 = time.perf_counter()
+        _, st = oracle.ls1_sort(keys)
+        t1 = time.perf_counter()
+        oracle.sort(keys)
+        t2 = time.perf_counter()
+        out[name] = {"ls1_s": round(t1 - t0, 3), "ls2_s": round(t2 - t1, 3),
+                     "ls2_over_ls1": round((t1 - t0) / (t2 - t1), 3),
+                     "ls1_spill_keys": st["spill_keys"], "ls1_exception_keys": st["exception_keys"]}
+    return out
 
 
 def lscpu():

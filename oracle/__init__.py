@@ -61,13 +61,28 @@ class Stats(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
+class LS1Config(C.Structure):
+    """ls1o_config (oracle/ls1_oracle.c)."""
+    _fields_ = [("fanout", C.c_uint32), ("leaf_count", C.c_uint32),
+                ("sample_stride", C.c_uint32), ("slack", C.c_double), ("cap0", C.c_uint64),
+                ("cap1", C.c_uint64), ("exc_min", C.c_uint64)]
+
+
+class LS1Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "spill_l0", "spill_keys", "exception_values", "exception_keys", "shifts", "guard_fired")]
+
+    def as_dict(self) -> dict:
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
 def build(force: bool = False) -> str:
     """Compile liboracle.so with plain gcc (no contraction, no fast-math)."""
-    src = os.path.join(_HERE, "ls2_oracle.c")
+    srcs = [os.path.join(_HERE, f) for f in ("ls2_oracle.c", "ls1_oracle.c")]
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
-            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "ls2_oracle.h"))):
+            [os.path.getmtime(x) for x in srcs] + [os.path.getmtime(os.path.join(_HERE, "ls2_oracle.h"))]):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-Wall", "-o", _SO, src, "-lm"])
+                               "-fPIC", "-shared", "-Wall", "-o", _SO] + srcs + ["-lm"])
     return _SO
 
 
@@ -140,6 +155,8 @@ def lib():
         L.lso_sort.argtypes = [P, C.c_uint64, C.c_int, C.POINTER(Config), C.POINTER(Model),
                                C.POINTER(Model), C.POINTER(Dumps), C.POINTER(Stats)]
         L.lso_reference_sort.argtypes = [P, C.c_uint64, C.c_int]
+        L.ls1o_config_default.argtypes = [C.POINTER(LS1Config)]
+        L.ls1o_sort.argtypes = [P, C.c_uint64, C.c_int, C.POINTER(LS1Config), C.POINTER(LS1Stats)]
         _lib = L
     return _lib
 
@@ -226,3 +243,21 @@ def reference_sort(keys: np.ndarray) -> np.ndarray:
     a = keys.copy()
     lib().lso_reference_sort(_u64(a).ctypes.data, len(a), dtype_code(keys))
     return a
+
+
+def ls1_config(fanout=1000, leaf_count=1000, sample_stride=100, slack=1.1, cap0=0, cap1=0,
+               exc_min=0) -> LS1Config:
+    return LS1Config(fanout, leaf_count, sample_stride, slack, cap0, cap1, exc_min)
+
+
+def ls1_sort(keys: np.ndarray, cfg: LS1Config | None = None):
+    """LearnedSort 1.0 (oracle variant) on a copy.
+    Returns (sorted, stats-dict)."""
+    a = keys.copy()
+    u = _u64(a)
+    st = LS1Stats()
+    rc = lib().ls1o_sort(u.ctypes.data, len(u), dtype_code(keys), C.byref(cfg or ls1_config()),
+                         C.byref(st))
+    if rc != OK:
+        raise OracleError(rc)
+    return a, st.as_dict()

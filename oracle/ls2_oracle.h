@@ -131,6 +131,28 @@ int lso_sort(uint64_t *A, uint64_t n, int dtype, const lso_config *cfg,
 /* The plain definition of the result: sort by ord (qsort). */
 void lso_reference_sort(uint64_t *A, uint64_t n, int dtype);
 
+/* ---- LearnedSort 1.0 as an oracle variant (ls1_oracle.c).
+ * Fixed-capacity buckets + spill bucket + exception table.
+ * Context only (the paper's LS 2.0 / LS 1.0 ratios); readings R-LS1a..d. */
+typedef struct {
+    uint32_t fanout, leaf_count, sample_stride;
+    double slack;     /* capacities = ceil(slack * expected size) (R-LS1a) */
+    uint64_t cap0;    /* level-0 bucket capacity; 0 = ceil(slack * n / f)     */
+    uint64_t cap1;    /* level-1 capacity; 0 = ceil(slack * cap0 / f)         */
+    uint64_t exc_min; /* sample count of a problematic key; 0 = max(2, ceil(m/f)) (R-LS1b) */
+} ls1o_config;
+
+typedef struct {
+    uint64_t spill_l0, spill_keys;          /* keys spilled at level 0 / in total   */
+    uint64_t exception_values, exception_keys; /* problematic keys: table entries / keys counted */
+    uint64_t shifts, guard_fired;
+} ls1o_stats;
+
+void ls1o_config_default(ls1o_config *cfg);
+/* Sorts A[0..n) in place. Returns LSO_OK, LSO_E_INVALID, LSO_E_NAN or
+ * LSO_E_INTERNAL. stats may be NULL. */
+int ls1o_sort(uint64_t *A, uint64_t n, int dtype, const ls1o_config *cfg, ls1o_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif
