@@ -44,7 +44,8 @@ struct Layout {
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
         cap0, bsrc, cur0, shist0,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist;
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist,
+        border;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
     uint64_t Bcap;
@@ -133,6 +134,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.big = take((size_t)(BIG_LEVELS + 1) * l.big_cap * sizeof(BigItem));
     l.chunk_cap = (uint32_t)(n / MM_CHUNK + l.big_cap + 1);
     l.chunks = take((size_t)l.chunk_cap * sizeof(BigChunk));
+    l.border = take((size_t)l.big_cap * 8);
     l.hist1_u64 = take(ff * 8);
     l.B = take((size_t)l.Bcap * 8);
     l.total = align_up(off, 256);
@@ -210,6 +212,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.task_cap = l.task_cap;
     a.big = (BigItem *)(w + l.big);
     a.chunks = (BigChunk *)(w + l.chunks);
+    a.border = (uint32_t *)(w + l.border);
     a.chunk_cap = l.chunk_cap;
     return a;
 }
@@ -371,6 +374,8 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     launches++;
     launch_large(a, dt, st);
     launches += 5;
+    launch_big_order(a, st);
+    launches++;
     launch_big(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_BIG);

@@ -294,6 +294,7 @@ struct Ctl {
     uint32_t ticket0, ticket1, U1;
     uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
+    uint32_t big_lv0;                  // level-0 tickets of k_big: level-0 items + the large path's level-1 items
     uint32_t nchunks;                  // k_big_minmax work entries
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
@@ -314,6 +315,8 @@ struct BigItem {
     uint32_t g;          // originating sub-bucket (for H1 dumps), or ~0u
     unsigned long long mn, mx;  // ord range (level 0: filled by k_big_minmax)
     uint32_t pad0, pad1;
+    unsigned long long dif;     // OR of ord(x) ^ ord(first key): its trailing zeros are the
+                                // low bits every key shares (the dense path's value stride)
 };
 constexpr uint32_t MM_CHUNK = 65536;
 struct BigChunk {
@@ -377,6 +380,7 @@ struct Args {
     uint32_t fcap;
     BigItem *big;                     // [(BIG_LEVELS+1) * big_cap]
     BigChunk *chunks;                 // [chunk_cap]
+    uint32_t *border;                 // [2 big_cap] k_big's first-pass items, most expensive first (k_big_order)
     uint32_t chunk_cap;
     // parity dumps (may be null)
     uint8_t *dH0, *dH1;
@@ -426,6 +430,11 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t *s, int len, uint32_t 
     return total;
 }
 
+__device__ __forceinline__ unsigned long long warp_or_u64(unsigned long long v) {
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+    return ((unsigned long long)hi << 32) | lo;
+}
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

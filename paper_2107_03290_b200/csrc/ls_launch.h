@@ -35,6 +35,7 @@ void launch_round1(const Args &a, int dtype, cudaStream_t st);
 // in-bucket sort (ls_sortsub.cu)
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);
+void launch_big_order(const Args &a, cudaStream_t st);
 void launch_big(const Args &a, int dtype, cudaStream_t st);  // all levels, one cooperative launch
 void launch_large(const Args &a, int dtype, cudaStream_t st);  // ls_bigpath.cu
 

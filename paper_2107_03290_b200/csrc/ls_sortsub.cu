@@ -1218,6 +1218,19 @@ constexpr int BIG_CHUNK = BIG_SORT_CAP / 2;
 constexpr int BIG_MAXWIN = 1024;       // windows classified per round
 constexpr int BIG_MAXBLK = 64;         // pieces in (BIG_CHUNK, BIG_SORT_CAP] per item
 constexpr int BIG_MAXWBIG = 16;        // pieces of 257..BIG_CHUNK keys per window (CTA-sorted)
+constexpr int BIG_DENSE_MAX = 49152;   // slots of the counting sort by value (16-bit counters alias sk..end)
+
+// The dense test of a non-homogeneous big item (mn != mx, so dif != 0):
+// every key is mn + s * 2^tz with s < nsl (tz = the low bits all keys share).
+__device__ __forceinline__ bool big_is_dense(uint32_t size, unsigned long long mn,
+                                             unsigned long long mx, unsigned long long dif,
+                                             int &tz, uint32_t &nsl) {
+    tz = __ffsll((long long)dif) - 1;
+    const unsigned long long s = ((mx - mn) >> tz) + 1ull;
+    nsl = (uint32_t)min(s, 0xffffffffull);
+    return size > (uint32_t)BIG_SORT_CAP && s <= (unsigned long long)BIG_DENSE_MAX;
+}
+
 
 // ord min/max of level-0 big items, one 64K-key chunk per work entry
 // (classify wrote the chunk list), so a multi-million-key homogeneous
@@ -1226,7 +1239,7 @@ constexpr int BIG_MAXWBIG = 16;        // pieces of 257..BIG_CHUNK keys per wind
 template <int DT>
 __global__ void __launch_bounds__(512) k_big_minmax(Args a) {
     if (a.ctl->status) return;
-    __shared__ unsigned long long red[64];
+    __shared__ unsigned long long red[96];
     const uint32_t nch = min(a.ctl->nchunks, a.chunk_cap);
     const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint32_t e = blockIdx.x; e < nch; e += gridDim.x) {
@@ -1234,42 +1247,96 @@ __global__ void __launch_bounds__(512) k_big_minmax(Args a) {
         const BigItem item = a.big[ch.item];
         const uint32_t beg = ch.chunk * MM_CHUNK, end = min(item.size, beg + MM_CHUNK);
         const uint64_t *X = a.A + item.off;
-        unsigned long long mn = ~0ull, mx = 0;
-        for (uint32_t i = beg + threadIdx.x; i < end; i += 4 * blockDim.x) {
-            uint64_t v[4];
+        const unsigned long long ref = to_ord<DT>(X[0]);  // (the item's first key: same for every chunk)
+        unsigned long long mn = ~0ull, mx = 0, dif = 0;
+        for (uint32_t i = beg + threadIdx.x; i < end; i += 8 * blockDim.x) {
+            uint64_t v[8];
 #pragma unroll
-            for (int q = 0; q < 4; q++) v[q] = (i + q * blockDim.x < end) ? X[i + q * blockDim.x] : X[beg];
+            for (int q = 0; q < 8; q++) v[q] = (i + q * blockDim.x < end) ? __ldcs(&X[i + q * blockDim.x]) : X[beg];
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
+            for (int q = 0; q < 8; q++) {
                 const unsigned long long o = to_ord<DT>(v[q]);
                 mn = o < mn ? o : mn;
                 mx = o > mx ? o : mx;
+                dif |= o ^ ref;
             }
         }
         mn = warp_min_u64(mn);
         mx = warp_max_u64(mx);
+        dif = warp_or_u64(dif);
         if ((threadIdx.x & 31) == 0) {
             red[w] = mn;
             red[32 + w] = mx;
+            red[64 + w] = dif;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int k = 1; k < nw; k++) {
                 mn = red[k] < mn ? red[k] : mn;
                 mx = red[32 + k] > mx ? red[32 + k] : mx;
+                dif |= red[64 + k];
             }
             atomicMin(&a.big[ch.item].mn, mn);
             atomicMax(&a.big[ch.item].mx, mx);
+            if (dif) atomicOr(&a.big[ch.item].dif, dif);
         }
         __syncthreads();
     }
 }
 
+// k_big's first pass takes the level-0 big items AND the level-1 items the
+// large path (ls_bigpath.cu, run before k_big) has already listed, in
+// decreasing estimated cost (one CTA; a counting sort on quarter-octaves of
+// the cost): the CTAs then finish together instead of waiting at the grid
+// barrier behind a late radix item, and the large path's ~100K-key pieces no
+// longer wait for a second pass of their own (config 4: ~500 dense + ~580
+// radix items of ~100K keys, 296 CTAs). Entry = level-0 index, or
+// 0x80000000 | level-1 index.
+constexpr int BO_CLASSES = 256;
+__global__ void __launch_bounds__(1024) k_big_order(Args a) {
+    if (a.ctl->status) return;
+    __shared__ uint32_t h[BO_CLASSES];
+    __shared__ uint32_t tmp[36];
+    const uint32_t cnt0 = min(a.ctl->big_cnt[0], a.big_cap);
+    const uint32_t pre1 = min(a.ctl->big_cnt[1], a.big_cap);
+    const uint32_t cnt = cnt0 + pre1;
+    for (int c = threadIdx.x; c < BO_CLASSES; c += blockDim.x) h[c] = 0;
+    __syncthreads();
+    auto cls = [&](uint32_t i) -> uint32_t {
+        double cost;
+        if (i < cnt0) {
+            const BigItem it = a.big[i];
+            if (it.mn == it.mx || it.pad0) return BO_CLASSES - 1;  // homogeneous / large path: nothing here
+            int tz;
+            uint32_t nsl;
+            const uint32_t w = big_is_dense(it.size, it.mn, it.mx, it.dif, tz, nsl) ? 1u
+                               : it.size <= (uint32_t)BIG_SORT_CAP                   ? 2u : 4u;
+            cost = (double)it.size * (double)w;
+        } else {  // level-1 item: min/max pass + radix
+            cost = (double)a.big[(size_t)a.big_cap + (i - cnt0)].size * 5.0;
+        }
+        const int q = (int)(__log2f((float)cost) * 4.0f);  // quarter octaves, 0..~150
+        return (uint32_t)max(0, BO_CLASSES - 2 - q);
+    };
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) atomicAdd(&h[cls(i)], 1u);
+    __syncthreads();
+    block_exscan(h, BO_CLASSES, tmp);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x)
+        a.border[atomicAdd(&h[cls(i)], 1u)] = i < cnt0 ? i : 0x80000000u | (i - cnt0);
+    if (threadIdx.x == 0) {
+        a.ctl->big_lv0 = cnt;
+        a.ctl->big_next[1] = pre1;  // (the second pass starts after them)
+    }
+}
+
 template <int DT>
 __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long &mn,
-                           unsigned long long &mx, unsigned long long *red) {
+                           unsigned long long &mx, unsigned long long &dif, unsigned long long *red) {
     mn = ~0ull;
     mx = 0;
+    dif = 0;
+    const unsigned long long ref = to_ord<DT>(X[0]);
     for (uint32_t i = threadIdx.x; i < size; i += 4 * blockDim.x) {
         uint64_t v[4];
 #pragma unroll
@@ -1279,21 +1346,26 @@ __device__ void big_minmax(const uint64_t *X, uint32_t size, unsigned long long 
             const unsigned long long o = to_ord<DT>(v[q]);
             mn = o < mn ? o : mn;
             mx = o > mx ? o : mx;
+            dif |= o ^ ref;
         }
     }
     mn = warp_min_u64(mn);
     mx = warp_max_u64(mx);
+    dif = warp_or_u64(dif);
     const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         red[w] = mn;
         red[32 + w] = mx;
+        red[64 + w] = dif;
     }
     __syncthreads();
     mn = red[0];
     mx = red[32];
+    dif = red[64];
     for (int i = 1; i < nw; i++) {
         mn = red[i] < mn ? red[i] : mn;
         mx = red[32 + i] > mx ? red[32 + i] : mx;
+        dif |= red[64 + i];
     }
     __syncthreads();
 }
@@ -1302,15 +1374,98 @@ static_assert(sizeof(BsSmem) * BS_CTAS_PER_SM <= 228 * 1024, "bucket sort shared
 
 struct BigSmem {
     uint64_t sk[BIG_SORT_CAP + 2];          // (+2: aligned hull of a TMA-staged window)
+    uint32_t start[BIG_DIGITS], end[BIG_DIGITS];  // (sk..end: the dense path's 16-bit counters)
     uint64_t mbar;
-    uint32_t start[BIG_DIGITS], end[BIG_DIGITS];
     uint32_t wlo[BIG_MAXWIN], whi[BIG_MAXWIN];
     uint32_t blk[BIG_MAXBLK];
     uint32_t wbig[BIG_MAXWBIG];             // window pieces of 257..BIG_CHUNK keys
     uint32_t tmp[36];
     uint32_t item, nblk, nwbig;
-    unsigned long long red[64];
+    unsigned long long red[96];
 };
+
+static_assert((BIG_SORT_CAP + 2) * 8 + 2 * BIG_DIGITS * 4 >= BIG_DENSE_MAX * 2, "dense counters fit sk..end");
+static_assert(2 * BIG_MAXWIN >= BIG_DENSE_MAX / 32, "dense chunk totals fit wlo..whi");
+
+// Counting sort by value of one big item whose keys are mn + s * 2^tz,
+// s < nsl <= BIG_DENSE_MAX: 16-bit slot counters (two per 32-bit word,
+// aliasing S.sk .. S.end), an exclusive scan, then every slot's value written
+// count times at its place. A slot with >= 2^16 keys would wrap its counter
+// and carry into (or past) its neighbour; every such wrap lowers the counter
+// total, so total == size proves there was none -- otherwise nothing has been
+// written and the caller sorts the item by radix (returns false). Ends with a
+// block barrier.
+template <int DT>
+__device__ __noinline__ bool big_dense(const uint64_t *__restrict__ X, uint64_t *__restrict__ out,
+                                       uint32_t size, unsigned long long mn, int tz, uint32_t nsl,
+                                       BigSmem &S, unsigned long long *prof) {
+    uint32_t *cw = reinterpret_cast<uint32_t *>(S.sk);
+    const uint16_t *cnt = reinterpret_cast<const uint16_t *>(S.sk);
+    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = bd >> 5;
+    long long t0 = clock64();
+    for (uint32_t w = tid; w < (nsl + 1) / 2; w += bd) cw[w] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < size; i += 8 * bd) {
+        uint64_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = (i + q * bd < size) ? X[i + q * bd] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (i + q * bd < size) {
+                const uint32_t s = (uint32_t)((to_ord<DT>(v[q]) - mn) >> tz);
+                atomicAdd(&cw[s >> 1], 1u << ((s & 1u) * 16u));
+            }
+    }
+    __syncthreads();
+    if (prof && tid == 0) { const long long t = clock64(); atomicAdd(&prof[6], (unsigned long long)(t - t0)); t0 = t; }
+    // chunks of 32 slots, dealt round-robin to the warps (a Gaussian cluster
+    // puts most keys in the middle chunks): chunk totals, their exclusive
+    // scan (in S.wlo, free here), then each chunk's runs
+    uint32_t *ctot = S.wlo;  // (wlo, whi: adjacent)
+    const uint32_t nch = (nsl + 31) / 32;
+    for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
+        const uint32_t k = 32 * c + (uint32_t)lane;
+        const uint32_t t = __reduce_add_sync(0xffffffffu, k < nsl ? (uint32_t)cnt[k] : 0u);
+        if (lane == 0) ctot[c] = t;
+    }
+    __syncthreads();
+    const uint32_t all = block_exscan(ctot, (int)nch, S.tmp);
+    __syncthreads();
+    if (all != size) return false;  // a counter wrapped: radix instead (uniform decision)
+    for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
+        const uint32_t s = 32 * c, k = s + (uint32_t)lane;
+        const uint32_t cc = k < nsl ? cnt[k] : 0u;
+        const uint32_t incl = warp_incl_scan(cc);
+        const uint32_t rel = incl - cc;  // run start relative to the chunk's first key
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t carry = ctot[c];
+        // the 32 slots' runs are contiguous: output position p belongs to the
+        // last slot j with rel_j <= p (an empty slot shares its start with the
+        // next non-empty one, which is later) -- a 5-step search over the lanes
+        for (uint32_t p0 = 0; p0 < total; p0 += 128) {  // (4 independent searches in flight)
+            uint32_t p[4], j[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                p[u] = p0 + 32u * u + (uint32_t)lane;
+                j[u] = 0;
+            }
+#pragma unroll
+            for (int b = 16; b > 0; b >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t r = __shfl_sync(0xffffffffu, rel, j[u] + b);
+                    j[u] = r <= p[u] ? j[u] + b : j[u];
+                }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (p[u] < total) out[carry + p[u]] = from_ord<DT>(mn + ((unsigned long long)(s + j[u]) << tz));
+        }
+    }
+    __syncthreads();  // (the counters alias S.sk: the next item may reuse it)
+    if (prof && tid == 0) atomicAdd(&prof[9], (unsigned long long)(clock64() - t0));
+    return true;
+}
 
 // One CTA per big item of this level: MSD radix partition X -> Y on the top
 // 12 bits of ord - min, then every piece is sorted exactly in shared memory
@@ -1323,8 +1478,7 @@ template <int DT>
 __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, uint32_t &mphase) {
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
-    const uint32_t cnt = min(*(volatile uint32_t *)&a.ctl->big_cnt[level], a.big_cap);
-    const BigItem *list = a.big + (size_t)level * a.big_cap;
+    const uint32_t cnt = level == 0 ? a.ctl->big_lv0 : min(*(volatile uint32_t *)&a.ctl->big_cnt[level], a.big_cap);
     const bool prof = (a.dbg & 512u) && threadIdx.x == 0;
     long long t_prev = clock64();
 #define BG_PROF(k)                                                                  \
@@ -1335,27 +1489,47 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
             t_prev = t_;                                                            \
         }                                                                           \
     } while (0)
+    long long t_it = 0;
+    uint32_t sz_it = 0;
+    auto rec_item = [&]() {  // (profiling: the previous item's duration, packed with its size)
+        if (prof && sz_it) {
+            const unsigned long long dur = (unsigned long long)(clock64() - t_it);
+            atomicMax(&a.ctl->prof[5], (dur << 32) | sz_it);
+        }
+    };
     for (;;) {
+        BG_PROF(10);
+        rec_item();
         if (tid == 0) S.item = atomicAdd(&a.ctl->big_next[level], 1u);
         __syncthreads();
         const uint32_t it = S.item;
         __syncthreads();
         if (it >= cnt) break;
-        const BigItem item = list[it];
+        int lv = level;  // the item's own level (the first pass mixes levels 0 and 1)
+        uint32_t ix = it;
+        if (level == 0) {
+            ix = a.border[it];
+            lv = ix >> 31;
+            ix &= 0x7fffffffu;
+        }
+        const BigItem item = a.big[(size_t)lv * a.big_cap + ix];
+        t_it = clock64();
+        sz_it = item.size;
         const uint64_t *X = (item.in_b ? a.B : a.A) + item.off;
         uint64_t *Y = (item.in_b ? a.A : a.B) + item.off;
         uint64_t *Aout = a.A + item.off;
-        unsigned long long mn, mx;
-        if (level == 0) {
+        unsigned long long mn, mx, dif;
+        if (lv == 0) {
             mn = item.mn;
             mx = item.mx;
+            dif = item.dif;
         } else {
-            big_minmax<DT>(X, item.size, mn, mx, S.red);
+            big_minmax<DT>(X, item.size, mn, mx, dif, S.red);
         }
         if (mn == mx) {  // homogeneous: already final
             if (item.in_b)
                 for (uint32_t i = tid; i < item.size; i += bd) Aout[i] = X[i];
-            if (tid == 0 && level == 0) {
+            if (tid == 0 && lv == 0) {
                 if (a.dH1) a.dH1[item.g] = 1;
                 atomicAdd(&a.ctl->stat[ST_H1S], 1ull);
                 atomicAdd(&a.ctl->stat[ST_H1K], (unsigned long long)item.size);
@@ -1364,15 +1538,33 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
             continue;
         }
         if (tid == 0) {
-            if (level == 0) {
+            if (lv == 0) {
                 atomicAdd(&a.ctl->stat[ST_BIGS], 1ull);
                 atomicAdd(&a.ctl->stat[ST_BIGK], (unsigned long long)item.size);
             }
             atomicAdd(&a.ctl->stat[ST_BIGPASS], 1ull);
         }
-        if (level == 0 && item.pad0) {  // large: sorted by ls_bigpath.cu
+        if (lv == 0 && item.pad0) {  // large: sorted by ls_bigpath.cu
             __syncthreads();
             continue;
+        }
+        // dense values: every key is mn + s * 2^tz with s < nslot (tz = the low
+        // bits all keys share). A counting sort BY VALUE is then exact: count
+        // the slots, scan, write every slot's value count times (16 B/key, no
+        // key moves; config 4's ID clusters: ~8K values in ~100K keys)
+        {
+            int tz;
+            uint32_t nsl;
+            if (big_is_dense(item.size, mn, mx, dif, tz, nsl)) {
+                BG_PROF(15);
+                const bool ok = big_dense<DT>(X, Aout, item.size, mn, tz, nsl, S, prof ? a.ctl->prof : nullptr);
+                BG_PROF(12);
+                if (ok) {
+                    if (prof) atomicAdd(&a.ctl->prof[13], 1ull);
+                    continue;
+                }
+            }
+            if (prof) atomicAdd(&a.ctl->prof[14], 1ull);
         }
         if (item.size <= BIG_SORT_CAP) {
             for (uint32_t i = tid; i < item.size; i += bd) S.sk[i] = X[i];
@@ -1477,10 +1669,10 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                     if (pc <= BIG_SORT_CAP) k = atomicAdd(&S.nblk, 1u);
                     if (k < BIG_MAXBLK) {
                         S.blk[k] = (uint32_t)d;
-                    } else if (level + 1 < BIG_LEVELS) {  // next level
-                        const uint32_t q = atomicAdd(&a.ctl->big_cnt[level + 1], 1u);
+                    } else if (lv + 1 < BIG_LEVELS) {  // next level
+                        const uint32_t q = atomicAdd(&a.ctl->big_cnt[lv + 1], 1u);
                         if (q < a.big_cap)
-                            a.big[(size_t)(level + 1) * a.big_cap + q] =
+                            a.big[(size_t)(lv + 1) * a.big_cap + q] =
                                 BigItem{item.off + ps, pc, y_is_b ? 1u : 0u, ~0u, ~0ull, 0ull, 0u, 0u};
                         else
                             atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
@@ -1511,10 +1703,8 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                         bulk_g2s((char *)S.sk + o, (const char *)(Yb + h0) + o,
                                  bytes - o < 32768u ? bytes - o : 32768u, &S.mbar);
                 }
-                BG_PROF(5);
                 mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
-                BG_PROF(6);
                 uint64_t *sk = S.sk + (gl & 1ull);
                 for (uint32_t d = dlo + tid; d <= dhi; d += bd) {  // one thread per tiny piece
                     const uint32_t pc = S.end[d] - S.start[d];
@@ -1523,8 +1713,6 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                 BG_PROF(7);
                 for (uint32_t d = dlo + warp; d <= dhi; d += nwarps) {  // one warp per larger piece
                     const uint32_t pc = S.end[d] - S.start[d];
-                    if ((a.dbg & 512u) && lane == 0 && pc > 1)
-                        atomicAdd(&a.ctl->prof[pc <= 8 ? 6 : pc <= 32 ? 7 : pc <= 64 ? 8 : pc <= 256 ? 9 : pc <= 1024 ? 10 : 11], 1ull);
                     if (pc <= 8) continue;
                     uint64_t *g = sk + (S.start[d] - slo);
                     if (shift <= 32 && pc <= 256) {  // piece within 2^32 ords: 32-bit peeling
@@ -1564,7 +1752,6 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                 if (tid == 0) S.nwbig = 0;  // for the next window (ordered by the barrier below)
                 for (uint32_t i = tid; i < shi - slo; i += bd) Aout[slo + i] = sk[i];
                 __syncthreads();
-                BG_PROF(9);
             }
         }
         BG_PROF(3);
@@ -1597,7 +1784,11 @@ __global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a) {
     for (int lv = 0; lv < BIG_LEVELS; lv++) {
         if (*(volatile uint32_t *)&a.ctl->big_cnt[lv] == 0) break;  // uniform: read after a grid barrier
         big_level<DT>(a, lv, S, mphase);
+        const long long t0 = clock64();
         grid.sync();
+        if ((a.dbg & 512u) && threadIdx.x == 0) {
+            atomicAdd(&a.ctl->prof[11], (unsigned long long)(clock64() - t0));
+        }
     }
 }
 
@@ -1647,6 +1838,8 @@ void launch_big_minmax(const Args &a, int dtype, cudaStream_t st) {
     if (dtype == DT_F64) k_big_minmax<DT_F64><<<148 * 4, 512, 0, st>>>(a);
     else k_big_minmax<DT_U64><<<148 * 4, 512, 0, st>>>(a);
 }
+
+void launch_big_order(const Args &a, cudaStream_t st) { k_big_order<<<1, 1024, 0, st>>>(a); }
 
 void launch_big(const Args &a, int dtype, cudaStream_t st) {
     const size_t sm = sizeof(BigSmem);

@@ -487,6 +487,49 @@ def test_large_big_items(case):
         assert st["big_keys"] >= 800_000
 
 
+def _dense_clusters(case, seed):
+    """20 clusters of 30K keys (BIG sub-buckets of 8K..256K keys: the per-CTA
+    big path) plus a uniform background. The cluster values decide whether the
+    counting sort by value (k_big's dense path: keys = mn + s * 2^tz with
+    fewer than 16K slots) or the MSD radix path sorts them."""
+    rng = np.random.default_rng(seed)
+    if case == "f64":                 # 6000 consecutive doubles per cluster (ord stride 1)
+        parts = [c + rng.integers(0, 6000, 30_000) * np.spacing(abs(c))
+                 for c in rng.uniform(-1e6, 1e6, 20)]
+        parts.append(rng.uniform(-1e6, 1e6, 200_001))
+        a = np.concatenate(parts)
+        rng.shuffle(a)
+        return a
+    centres = rng.integers(2 ** 40, 2 ** 62, 20)
+    parts = []
+    for j, c in enumerate(centres):
+        if case == "stride1024":      # config 4's fp64-built IDs: multiples of 2^10, ~8K slots
+            k = np.clip(np.rint(rng.normal(0, 1024, 30_000)), -4000, 4000).astype(np.int64)
+            v = np.uint64(c & ~1023) + (k * 1024).astype(np.uint64)
+        elif case == "stride1":       # consecutive integers, 10K slots
+            v = np.uint64(c) + rng.integers(0, 10_000, 30_000).astype(np.uint64)
+        elif case == "wide":          # 50K slots: radix path
+            v = np.uint64(c) + rng.integers(0, 50_000, 30_000).astype(np.uint64)
+        elif case == "mixed":         # one cluster in two breaks the stride with a single odd key
+            v = np.uint64(c & ~1023) + (rng.integers(0, 8000, 30_000) * 1024).astype(np.uint64)
+            if j % 2:
+                v[7] += np.uint64(1)
+        parts.append(v.astype(np.uint64))
+    parts.append(rng.integers(0, 2 ** 63, 200_001, dtype=np.uint64))
+    a = np.concatenate(parts)
+    rng.shuffle(a)
+    return a
+
+
+@pytest.mark.parametrize("case", ["stride1024", "stride1", "wide", "mixed", "f64"])
+def test_dense_big_items(case):
+    """k_big's counting sort by value (dense slots) and its radix fallback:
+    the oracle's output, S_B/S'_B/H0/H1 and the class counts."""
+    keys = from_np(_dense_clusters(case, 11))
+    st, ost = check_sort(keys)
+    assert st["big_keys"] >= 400_000
+
+
 # ------------------------------------------- the paper's second workloads --
 
 @pytest.mark.parametrize("s", [0.5, 0.9, 0.99])
