@@ -692,6 +692,8 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
         for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
         fprintf(stderr, "\ntasks: warp %u cta4096 %u cta2048 %u cta1024 %u windows %u large %u\n",
                 c.ntask, c.nctask, c.nctask2, c.nctask3, c.nwin, c.nlarge);
+        fprintf(stderr, "big items per level: %u %u %u %u (first pass %u)\n", c.big_cnt[0], c.big_cnt[1],
+                c.big_cnt[2], c.big_cnt[3], c.big_lv0);
         if (pend->model_dev) {
             uint32_t ns = 0;
             cudaMemcpy(&ns, &pend->model_dev->nsub, 4, cudaMemcpyDeviceToHost);

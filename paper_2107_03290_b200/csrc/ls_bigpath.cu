@@ -38,6 +38,7 @@ __device__ __forceinline__ int large_shift(unsigned long long mn, unsigned long 
 template <int DT>
 __global__ void __launch_bounds__(512) k_large_count(Args a) {
     if (a.ctl->status) return;
+    if (a.ctl->nlarge == 0) return;  // (no large item: skip the chunk list)
     __shared__ uint32_t hist[LD_DIG];
     __shared__ unsigned long long dmn[LD_DIG], dmx[LD_DIG];
     const uint32_t nch = min(a.ctl->nchunks, a.chunk_cap);
@@ -169,6 +170,7 @@ static_assert(sizeof(LargeSmem) <= MAX_SMEM_OPTIN, "large scatter shared memory"
 template <int DT>
 __global__ void __launch_bounds__(TP_THREADS, 1) k_large_scatter(Args a) {
     if (a.ctl->status) return;
+    if (a.ctl->nlarge == 0) return;  // (no large item: skip the chunk list)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LargeSmem &S = *reinterpret_cast<LargeSmem *>(smem_raw);
     const int tid = threadIdx.x;

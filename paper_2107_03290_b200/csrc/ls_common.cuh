@@ -295,6 +295,7 @@ struct Ctl {
     uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
     uint32_t big_lv0;                  // level-0 tickets of k_big: level-0 items + the large path's level-1 items
+    uint32_t big_pub1, big_done0;      // level-1 items published (in order) / first-pass tickets done
     uint32_t nchunks;                  // k_big_minmax work entries
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
@@ -430,6 +431,11 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t *s, int len, uint32_t 
     return total;
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __device__ __forceinline__ unsigned long long warp_or_u64(unsigned long long v) {
     const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
     const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));

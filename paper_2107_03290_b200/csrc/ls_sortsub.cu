@@ -1211,7 +1211,7 @@ __global__ void k_window_list(Args a) {
 }
 
 // ------------------------------------------------------------- BIG path ----
-constexpr int BIG_THREADS = 512;
+constexpr int BIG_THREADS = 1024;     // one CTA per SM: an item finishes twice as fast (shorter critical path)
 constexpr int BIG_DIGITS = 4096;       // 12-bit MSD digits
 constexpr int BIG_SORT_CAP = 8192;     // keys sorted in shared memory by one CTA
 constexpr int BIG_CHUNK = BIG_SORT_CAP / 2;
@@ -1219,16 +1219,18 @@ constexpr int BIG_MAXWIN = 1024;       // windows classified per round
 constexpr int BIG_MAXBLK = 64;         // pieces in (BIG_CHUNK, BIG_SORT_CAP] per item
 constexpr int BIG_MAXWBIG = 16;        // pieces of 257..BIG_CHUNK keys per window (CTA-sorted)
 constexpr int BIG_DENSE_MAX = 49152;   // slots of the counting sort by value (16-bit counters alias sk..end)
+constexpr int BIG_DENSE_WIN = 4;       // windows of BIG_DENSE_MAX slots (one pass over the item each)
 
 // The dense test of a non-homogeneous big item (mn != mx, so dif != 0):
 // every key is mn + s * 2^tz with s < nsl (tz = the low bits all keys share).
 __device__ __forceinline__ bool big_is_dense(uint32_t size, unsigned long long mn,
                                              unsigned long long mx, unsigned long long dif,
                                              int &tz, uint32_t &nsl) {
-    tz = __ffsll((long long)dif) - 1;
+    tz = dif ? __ffsll((long long)dif) - 1 : 32;  // (k_big_minmax ORs 32-bit differences: 0 -> >= 32 shared bits)
+    tz = min(tz, 32);
     const unsigned long long s = ((mx - mn) >> tz) + 1ull;
     nsl = (uint32_t)min(s, 0xffffffffull);
-    return size > (uint32_t)BIG_SORT_CAP && s <= (unsigned long long)BIG_DENSE_MAX;
+    return size > (uint32_t)BIG_SORT_CAP && s <= (unsigned long long)BIG_DENSE_MAX * BIG_DENSE_WIN;
 }
 
 
@@ -1237,48 +1239,61 @@ __device__ __forceinline__ bool big_is_dense(uint32_t size, unsigned long long m
 // sub-bucket (Zipf's top value, config 4's top level) is scanned by the whole
 // GPU instead of one CTA.
 template <int DT>
-__global__ void __launch_bounds__(512) k_big_minmax(Args a) {
+__global__ void __launch_bounds__(512, 3) k_big_minmax(Args a) {
     if (a.ctl->status) return;
-    __shared__ unsigned long long red[96];
+    __shared__ unsigned long long red[64];
+    __shared__ uint32_t redd[32];
     const uint32_t nch = min(a.ctl->nchunks, a.chunk_cap);
     const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t bd = blockDim.x;
     for (uint32_t e = blockIdx.x; e < nch; e += gridDim.x) {
         const BigChunk ch = a.chunks[e];
         const BigItem item = a.big[ch.item];
         const uint32_t beg = ch.chunk * MM_CHUNK, end = min(item.size, beg + MM_CHUNK);
         const uint64_t *X = a.A + item.off;
-        const unsigned long long ref = to_ord<DT>(X[0]);  // (the item's first key: same for every chunk)
-        unsigned long long mn = ~0ull, mx = 0, dif = 0;
-        for (uint32_t i = beg + threadIdx.x; i < end; i += 8 * blockDim.x) {
+        // dif: OR of the low 32 bits of ord ^ ord(first key): its trailing
+        // zeros (32 if none) are low bits every key shares (the dense path's
+        // value stride)
+        const uint32_t ref = (uint32_t)to_ord<DT>(X[0]);
+        uint32_t dif = 0;
+        unsigned long long mn = ~0ull, mx = 0;
+        uint32_t i = beg + threadIdx.x;
+        for (; i + 7 * bd < end; i += 8 * bd) {  // full rounds: 8 independent loads in flight
             uint64_t v[8];
 #pragma unroll
-            for (int q = 0; q < 8; q++) v[q] = (i + q * blockDim.x < end) ? __ldcs(&X[i + q * blockDim.x]) : X[beg];
+            for (int q = 0; q < 8; q++) v[q] = X[i + q * bd];
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 const unsigned long long o = to_ord<DT>(v[q]);
                 mn = o < mn ? o : mn;
                 mx = o > mx ? o : mx;
-                dif |= o ^ ref;
+                dif |= (uint32_t)o ^ ref;
             }
+        }
+        for (; i < end; i += bd) {
+            const unsigned long long o = to_ord<DT>(X[i]);
+            mn = o < mn ? o : mn;
+            mx = o > mx ? o : mx;
+            dif |= (uint32_t)o ^ ref;
         }
         mn = warp_min_u64(mn);
         mx = warp_max_u64(mx);
-        dif = warp_or_u64(dif);
+        dif = __reduce_or_sync(0xffffffffu, dif);
         if ((threadIdx.x & 31) == 0) {
             red[w] = mn;
             red[32 + w] = mx;
-            red[64 + w] = dif;
+            redd[w] = dif;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int k = 1; k < nw; k++) {
                 mn = red[k] < mn ? red[k] : mn;
                 mx = red[32 + k] > mx ? red[32 + k] : mx;
-                dif |= red[64 + k];
+                dif |= redd[k];
             }
             atomicMin(&a.big[ch.item].mn, mn);
             atomicMax(&a.big[ch.item].mx, mx);
-            if (dif) atomicOr(&a.big[ch.item].dif, dif);
+            if (dif) atomicOr(&a.big[ch.item].dif, (unsigned long long)dif);
         }
         __syncthreads();
     }
@@ -1292,25 +1307,55 @@ __global__ void __launch_bounds__(512) k_big_minmax(Args a) {
 // longer wait for a second pass of their own (config 4: ~500 dense + ~580
 // radix items of ~100K keys, 296 CTAs). Entry = level-0 index, or
 // 0x80000000 | level-1 index.
+static_assert(sizeof(BigItem) == 48, "BigItem is read as three 16-byte words");
 constexpr int BO_CLASSES = 256;
 __global__ void __launch_bounds__(1024) k_big_order(Args a) {
     if (a.ctl->status) return;
     __shared__ uint32_t h[BO_CLASSES];
     __shared__ uint32_t tmp[36];
+    __shared__ unsigned long long st[5];  // H1 sub-buckets / keys, big / big keys / passes of the skipped items
     const uint32_t cnt0 = min(a.ctl->big_cnt[0], a.big_cap);
     const uint32_t pre1 = min(a.ctl->big_cnt[1], a.big_cap);
     const uint32_t cnt = cnt0 + pre1;
     for (int c = threadIdx.x; c < BO_CLASSES; c += blockDim.x) h[c] = 0;
+    if (threadIdx.x < 5) st[threadIdx.x] = 0;
     __syncthreads();
+    // homogeneous level-0 items (final as they are) and large ones
+    // (ls_bigpath.cu) get no ticket: their statistics are counted here
+    {
+        uint32_t hs = 0, ls_ = 0;
+        unsigned long long hk = 0, lk = 0;
+        for (uint32_t i = threadIdx.x; i < cnt0; i += blockDim.x) {
+            const BigItem it = a.big[i];
+            if (it.mn == it.mx) {
+                if (a.dH1) a.dH1[it.g] = 1;
+                hs++;
+                hk += it.size;
+            } else if (it.pad0) {
+                ls_++;
+                lk += it.size;
+            }
+        }
+        // (warp sums first: one shared-memory atomic per warp, not per item)
+        hs = __reduce_add_sync(0xffffffffu, hs);
+        ls_ = __reduce_add_sync(0xffffffffu, ls_);
+        hk = warp_sum_u64(hk);
+        lk = warp_sum_u64(lk);
+        if ((threadIdx.x & 31) == 0) {
+            if (hs) { atomicAdd(&st[0], (unsigned long long)hs); atomicAdd(&st[1], hk); }
+            if (ls_) { atomicAdd(&st[2], (unsigned long long)ls_); atomicAdd(&st[3], lk); }
+        }
+    }
     auto cls = [&](uint32_t i) -> uint32_t {
         double cost;
         if (i < cnt0) {
             const BigItem it = a.big[i];
-            if (it.mn == it.mx || it.pad0) return BO_CLASSES - 1;  // homogeneous / large path: nothing here
+            if (it.mn == it.mx || it.pad0) return BO_CLASSES - 1;  // homogeneous / large path: no ticket
             int tz;
             uint32_t nsl;
-            const uint32_t w = big_is_dense(it.size, it.mn, it.mx, it.dif, tz, nsl) ? 1u
-                               : it.size <= (uint32_t)BIG_SORT_CAP                   ? 2u : 4u;
+            const uint32_t w = big_is_dense(it.size, it.mn, it.mx, it.dif, tz, nsl)
+                                   ? (nsl + BIG_DENSE_MAX - 1) / BIG_DENSE_MAX  // one pass per window
+                                   : it.size <= (uint32_t)BIG_SORT_CAP ? 2u : 5u;
             cost = (double)it.size * (double)w;
         } else {  // level-1 item: min/max pass + radix
             cost = (double)a.big[(size_t)a.big_cap + (i - cnt0)].size * 5.0;
@@ -1320,13 +1365,25 @@ __global__ void __launch_bounds__(1024) k_big_order(Args a) {
     };
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) atomicAdd(&h[cls(i)], 1u);
     __syncthreads();
+    const uint32_t nskip = h[BO_CLASSES - 1];
     block_exscan(h, BO_CLASSES, tmp);
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x)
-        a.border[atomicAdd(&h[cls(i)], 1u)] = i < cnt0 ? i : 0x80000000u | (i - cnt0);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const uint32_t c = cls(i);
+        if (c != BO_CLASSES - 1) a.border[atomicAdd(&h[c], 1u)] = i < cnt0 ? i : 0x80000000u | (i - cnt0);
+    }
     if (threadIdx.x == 0) {
-        a.ctl->big_lv0 = cnt;
-        a.ctl->big_next[1] = pre1;  // (the second pass starts after them)
+        if (st[0]) atomicAdd(&a.ctl->stat[ST_H1S], st[0]);
+        if (st[1]) atomicAdd(&a.ctl->stat[ST_H1K], st[1]);
+        if (st[2]) {
+            atomicAdd(&a.ctl->stat[ST_BIGS], st[2]);
+            atomicAdd(&a.ctl->stat[ST_BIGK], st[3]);
+            atomicAdd(&a.ctl->stat[ST_BIGPASS], st[2]);
+        }
+        a.ctl->big_lv0 = cnt - nskip;
+        a.ctl->big_next[1] = pre1;  // (consumed by the first pass's dynamic phase after them)
+        a.ctl->big_pub1 = pre1;
+        a.ctl->big_done0 = 0;
     }
 }
 
@@ -1397,72 +1454,95 @@ static_assert(2 * BIG_MAXWIN >= BIG_DENSE_MAX / 32, "dense chunk totals fit wlo.
 // block barrier.
 template <int DT>
 __device__ __noinline__ bool big_dense(const uint64_t *__restrict__ X, uint64_t *__restrict__ out,
-                                       uint32_t size, unsigned long long mn, int tz, uint32_t nsl,
-                                       BigSmem &S, unsigned long long *prof) {
+                                       uint64_t *__restrict__ scratch, uint32_t size,
+                                       unsigned long long mn, int tz, uint32_t nsl, BigSmem &S,
+                                       unsigned long long *prof) {
     uint32_t *cw = reinterpret_cast<uint32_t *>(S.sk);
     const uint16_t *cnt = reinterpret_cast<const uint16_t *>(S.sk);
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
+    // more than one window of slots: X is read once per window, so when X is
+    // `out` the runs go to the item's scratch range (which is not X) and are
+    // copied to `out` at the end
+    const bool multi = nsl > (uint32_t)BIG_DENSE_MAX && X == out;  // (X != out: write out directly)
+    uint64_t *dst = multi ? scratch : out;
+    uint32_t obase = 0;
     long long t0 = clock64();
-    for (uint32_t w = tid; w < (nsl + 1) / 2; w += bd) cw[w] = 0;
-    __syncthreads();
-    for (uint32_t i = tid; i < size; i += 8 * bd) {
-        uint64_t v[8];
+    for (uint32_t wb = 0; wb < nsl; wb += BIG_DENSE_MAX) {
+        const uint32_t wn = min((uint32_t)BIG_DENSE_MAX, nsl - wb);
+        for (uint32_t w = tid; w < (wn + 1) / 2; w += bd) cw[w] = 0;
+        __syncthreads();
+        uint32_t inw = 0;  // keys of this window seen by this thread
+        for (uint32_t i = tid; i < size; i += 8 * bd) {
+            uint64_t v[8];
 #pragma unroll
-        for (int q = 0; q < 8; q++) v[q] = (i + q * bd < size) ? X[i + q * bd] : 0;
+            for (int q = 0; q < 8; q++) v[q] = (i + q * bd < size) ? X[i + q * bd] : 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++)
-            if (i + q * bd < size) {
-                const uint32_t s = (uint32_t)((to_ord<DT>(v[q]) - mn) >> tz);
-                atomicAdd(&cw[s >> 1], 1u << ((s & 1u) * 16u));
-            }
-    }
-    __syncthreads();
-    if (prof && tid == 0) { const long long t = clock64(); atomicAdd(&prof[6], (unsigned long long)(t - t0)); t0 = t; }
-    // chunks of 32 slots, dealt round-robin to the warps (a Gaussian cluster
-    // puts most keys in the middle chunks): chunk totals, their exclusive
-    // scan (in S.wlo, free here), then each chunk's runs
-    uint32_t *ctot = S.wlo;  // (wlo, whi: adjacent)
-    const uint32_t nch = (nsl + 31) / 32;
-    for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
-        const uint32_t k = 32 * c + (uint32_t)lane;
-        const uint32_t t = __reduce_add_sync(0xffffffffu, k < nsl ? (uint32_t)cnt[k] : 0u);
-        if (lane == 0) ctot[c] = t;
-    }
-    __syncthreads();
-    const uint32_t all = block_exscan(ctot, (int)nch, S.tmp);
-    __syncthreads();
-    if (all != size) return false;  // a counter wrapped: radix instead (uniform decision)
-    for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
-        const uint32_t s = 32 * c, k = s + (uint32_t)lane;
-        const uint32_t cc = k < nsl ? cnt[k] : 0u;
-        const uint32_t incl = warp_incl_scan(cc);
-        const uint32_t rel = incl - cc;  // run start relative to the chunk's first key
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t carry = ctot[c];
-        // the 32 slots' runs are contiguous: output position p belongs to the
-        // last slot j with rel_j <= p (an empty slot shares its start with the
-        // next non-empty one, which is later) -- a 5-step search over the lanes
-        for (uint32_t p0 = 0; p0 < total; p0 += 128) {  // (4 independent searches in flight)
-            uint32_t p[4], j[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                p[u] = p0 + 32u * u + (uint32_t)lane;
-                j[u] = 0;
-            }
-#pragma unroll
-            for (int b = 16; b > 0; b >>= 1)
+            for (int q = 0; q < 8; q++)
+                if (i + q * bd < size) {
+                    const uint32_t s = (uint32_t)((to_ord<DT>(v[q]) - mn) >> tz) - wb;
+                    if (s < wn) {
+                        atomicAdd(&cw[s >> 1], 1u << ((s & 1u) * 16u));
+                        inw++;
+                    }
+                }
+        }
+        inw = __reduce_add_sync(0xffffffffu, inw);
+        if (lane == 0) S.tmp[warp] = inw;
+        __syncthreads();
+        uint32_t want = 0;
+        for (int w = 0; w < nwarps; w++) want += S.tmp[w];
+        if (prof && tid == 0) { const long long t = clock64(); atomicAdd(&prof[6], (unsigned long long)(t - t0)); t0 = t; }
+        // chunks of 32 slots, dealt round-robin to the warps (a Gaussian
+        // cluster puts most keys in the middle chunks): chunk totals, their
+        // exclusive scan (in S.wlo, free here), then each chunk's runs
+        uint32_t *ctot = S.wlo;  // (wlo, whi: adjacent)
+        const uint32_t nch = (wn + 31) / 32;
+        for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
+            const uint32_t k = 32 * c + (uint32_t)lane;
+            const uint32_t t = __reduce_add_sync(0xffffffffu, k < wn ? (uint32_t)cnt[k] : 0u);
+            if (lane == 0) ctot[c] = t;
+        }
+        __syncthreads();
+        const uint32_t all = block_exscan(ctot, (int)nch, S.tmp);
+        __syncthreads();
+        if (all != want) return false;  // a counter wrapped: radix instead (uniform decision; out untouched)
+        for (uint32_t c = (uint32_t)warp; c < nch; c += (uint32_t)nwarps) {
+            const uint32_t s = 32 * c, k = s + (uint32_t)lane;
+            const uint32_t cc = k < wn ? cnt[k] : 0u;
+            const uint32_t incl = warp_incl_scan(cc);
+            const uint32_t rel = incl - cc;  // run start relative to the chunk's first key
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t carry = obase + ctot[c];
+            // the 32 slots' runs are contiguous: output position p belongs to
+            // the last slot j with rel_j <= p (an empty slot shares its start
+            // with the next non-empty one, which is later) -- a 5-step search
+            for (uint32_t p0 = 0; p0 < total; p0 += 128) {  // (4 independent searches in flight)
+                uint32_t p[4], j[4];
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const uint32_t r = __shfl_sync(0xffffffffu, rel, j[u] + b);
-                    j[u] = r <= p[u] ? j[u] + b : j[u];
+                    p[u] = p0 + 32u * u + (uint32_t)lane;
+                    j[u] = 0;
                 }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (p[u] < total) out[carry + p[u]] = from_ord<DT>(mn + ((unsigned long long)(s + j[u]) << tz));
+                for (int b = 16; b > 0; b >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t r = __shfl_sync(0xffffffffu, rel, j[u] + b);
+                        j[u] = r <= p[u] ? j[u] + b : j[u];
+                    }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (p[u] < total)
+                        dst[carry + p[u]] = from_ord<DT>(mn + ((unsigned long long)(wb + s + j[u]) << tz));
+            }
         }
+        obase += want;
+        __syncthreads();  // (the counters alias S.sk: the next window / item reuses it)
     }
-    __syncthreads();  // (the counters alias S.sk: the next item may reuse it)
+    if (multi)
+        for (uint32_t i = tid; i < size; i += bd) out[i] = dst[i];
+    __syncthreads();
     if (prof && tid == 0) atomicAdd(&prof[9], (unsigned long long)(clock64() - t0));
     return true;
 }
@@ -1497,22 +1577,80 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
             atomicMax(&a.ctl->prof[5], (dur << 32) | sz_it);
         }
     };
+    // First pass (level 0): the first-pass tickets (k_big_order's list), then
+    // the level-1 items those items create, as soon as they are published
+    // (in order, big_pub1) -- no grid barrier between the two, so the pieces
+    // of a multi-cluster sub-bucket do not wait for the slowest CTA. Level 1
+    // is complete once every first-pass ticket is done (big_done0 == cnt).
+    bool dyn = false, counted = true;
+    constexpr uint32_t BI_END = 0xffffffffu, BI_DYN = 0x80000000u;
     for (;;) {
         BG_PROF(10);
         rec_item();
-        if (tid == 0) S.item = atomicAdd(&a.ctl->big_next[level], 1u);
+        if (tid == 0) {
+            if (!counted) {  // the previous first-pass ticket is done (its appends are published)
+                __threadfence();
+                atomicAdd(&a.ctl->big_done0, 1u);
+                counted = true;
+            }
+            uint32_t code = BI_END;
+            if (level != 0) {
+                const uint32_t t = atomicAdd(&a.ctl->big_next[level], 1u);
+                code = t < cnt ? t : BI_END;
+            } else {
+                if (!dyn) {
+                    const uint32_t t = atomicAdd(&a.ctl->big_next[0], 1u);
+                    if (t < cnt) {
+                        code = t;
+                        counted = false;
+                    } else {
+                        dyn = true;
+                    }
+                }
+                if (dyn) {
+                    const uint32_t t = atomicAdd(&a.ctl->big_next[1], 1u);
+                    for (;;) {
+                        if (t < *(volatile uint32_t *)&a.ctl->big_pub1) { code = BI_DYN | t; break; }
+                        if (*(volatile uint32_t *)&a.ctl->big_done0 == cnt) {
+                            __threadfence();
+                            code = t < *(volatile uint32_t *)&a.ctl->big_pub1 ? (BI_DYN | t) : BI_END;
+                            break;
+                        }
+                        __nanosleep(256);
+                    }
+                }
+            }
+            S.item = code;
+        }
         __syncthreads();
         const uint32_t it = S.item;
         __syncthreads();
-        if (it >= cnt) break;
+        if (it == BI_END) break;
         int lv = level;  // the item's own level (the first pass mixes levels 0 and 1)
         uint32_t ix = it;
         if (level == 0) {
-            ix = a.border[it];
-            lv = ix >> 31;
-            ix &= 0x7fffffffu;
+            if (it & BI_DYN) {
+                lv = 1;
+                ix = it & ~BI_DYN;
+            } else {
+                ix = a.border[it];
+                lv = ix >> 31;
+                ix &= 0x7fffffffu;
+            }
         }
-        const BigItem item = a.big[(size_t)lv * a.big_cap + ix];
+        if (lv != 0 && ix >= a.big_cap) {  // (a list overflow: status is set)
+            __syncthreads();
+            continue;
+        }
+        BigItem item;
+        {  // (published by another SM during this kernel: read through L2)
+            const BigItem *src = a.big + (size_t)lv * a.big_cap + ix;
+            const uint4 w0 = __ldcg(reinterpret_cast<const uint4 *>(src));
+            const uint4 w1 = __ldcg(reinterpret_cast<const uint4 *>(src) + 1);
+            const uint4 w2 = __ldcg(reinterpret_cast<const uint4 *>(src) + 2);
+            const uint4 ww[3] = {w0, w1, w2};
+            memcpy(&item, ww, sizeof item);
+        }
         t_it = clock64();
         sz_it = item.size;
         const uint64_t *X = (item.in_b ? a.B : a.A) + item.off;
@@ -1557,7 +1695,8 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
             uint32_t nsl;
             if (big_is_dense(item.size, mn, mx, dif, tz, nsl)) {
                 BG_PROF(15);
-                const bool ok = big_dense<DT>(X, Aout, item.size, mn, tz, nsl, S, prof ? a.ctl->prof : nullptr);
+                const bool ok = big_dense<DT>(X, Aout, a.B + item.off, item.size, mn, tz, nsl, S,
+                                              prof ? a.ctl->prof : nullptr);
                 BG_PROF(12);
                 if (ok) {
                     if (prof) atomicAdd(&a.ctl->prof[13], 1ull);
@@ -1676,6 +1815,11 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
                                 BigItem{item.off + ps, pc, y_is_b ? 1u : 0u, ~0u, ~0ull, 0ull, 0u, 0u};
                         else
                             atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+                        if (lv == 0) {  // level 1 is consumed during the first pass: publish in order
+                            __threadfence();
+                            while (atomicCAS(&a.ctl->big_pub1, q, q + 1u) != q) {
+                            }
+                        }
                     } else {
                         atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
                     }
@@ -1773,7 +1917,7 @@ __device__ __forceinline__ void big_level(const Args &a, int level, BigSmem &S, 
 // complete after a grid barrier; the kernel stops at the first empty level
 // (for smooth inputs: at once), instead of BIG_LEVELS separate launches.
 template <int DT>
-__global__ void __launch_bounds__(BIG_THREADS, 2) k_big(Args a) {
+__global__ void __launch_bounds__(BIG_THREADS, 1) k_big(Args a) {
     if (a.ctl->status) return;  // (set before this kernel: uniform across the grid)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BigSmem &S = *reinterpret_cast<BigSmem *>(smem_raw);
@@ -1835,8 +1979,11 @@ void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
 }
 
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st) {
-    if (dtype == DT_F64) k_big_minmax<DT_F64><<<148 * 4, 512, 0, st>>>(a);
-    else k_big_minmax<DT_U64><<<148 * 4, 512, 0, st>>>(a);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dtype == DT_F64) k_big_minmax<DT_F64><<<sms * 3, 512, 0, st>>>(a);  // (3 resident per SM: one wave)
+    else k_big_minmax<DT_U64><<<sms * 3, 512, 0, st>>>(a);
 }
 
 void launch_big_order(const Args &a, cudaStream_t st) { k_big_order<<<1, 1024, 0, st>>>(a); }
