@@ -163,6 +163,38 @@ __device__ __forceinline__ double predict_ldg_inner(uint64_t bits, const Root &R
     return __dadd_rn(clampd(y, __ldg(q + 3), __ldg(q + 4)), 0.0);
 }
 
+// The leaf that holds every key of sub-bucket g, + 1 (0: none). The model is
+// monotone-safe (model_ok: a >= 0, lo_l <= hi_l <= lo_{l+1}), so a key of
+// leaf m < l has p <= lo_l and a key of leaf m > l has p >= hi_l. A key of
+// sub-bucket g has p within 1e-15 of [g/f^2, (g+1)/f^2) (p * f^2 < 2^20 is
+// rounded by at most 2^-33). So if lo_l < g/f^2 - 1e-12 and (g+1)/f^2 +
+// 1e-12 < hi_l, every key of g comes from leaf l and its line value y lies in
+// (lo_l, hi_l): p = clamp(y) + 0 = y, with neither the routing, the clamp nor
+// the -0.0 canonicalisation needed (the warp sort's fast path). Keys outside
+// [xmin, xmax] (the root clamp) only reach the sub-buckets of xmin and xmax,
+// which the warp sort excludes.
+// One call per warp (all lanes, lane j asks for g = g0 + j): the last leaf
+// with lo < P0(g0) by two ballot rounds of 32 leaves (L <= LS_MAX_LEAVES =
+// 1024), then every lane walks up from it (consecutive sub-buckets: usually
+// 0-1 steps).
+static_assert(LS_MAX_LEAVES <= 1024, "contained_leaf_warp searches 32 x 32 leaves");
+__device__ __forceinline__ uint32_t contained_leaf_warp(const double *leaf, int L, uint32_t g0, uint32_t g,
+                                                        double rcpF2, int lane) {
+    // (rcpF2 = RN(1/f^2): g * rcpF2 is within 2 ulps of g/f^2, far inside the margin)
+    const double Q0 = __dsub_rn(__dmul_rn((double)g0, rcpF2), 1e-12);
+    const int l1 = 32 * lane;
+    const unsigned m1 = __ballot_sync(0xffffffffu, l1 < L && __ldg(leaf + 5 * l1 + 3) < Q0);
+    if (!m1) return 0u;  // (no leaf below: the first sub-buckets take the slow path)
+    const int blk = 31 - __clz(m1);
+    const int l2 = 32 * blk + lane;
+    const unsigned m2 = __ballot_sync(0xffffffffu, l2 < L && __ldg(leaf + 5 * l2 + 3) < Q0);
+    int l = 32 * blk + (31 - __clz(m2));  // (bit 0 of m2 is set: leaf 32*blk passed round 1)
+    const double P0 = __dsub_rn(__dmul_rn((double)g, rcpF2), 1e-12);
+    const double P1 = __dadd_rn(__dmul_rn((double)(g + 1u), rcpF2), 1e-12);
+    while (l + 1 < L && __ldg(leaf + 5 * (l + 1) + 3) < P0) l++;
+    return P1 < __ldg(leaf + 5 * l + 4) ? (uint32_t)l + 1u : 0u;
+}
+
 // O7 / Alg.1 P:107 (R1)
 // (p in [0, 1) and f <= 1024, so p * f^2 < 2^20: a 32-bit truncation is the
 // same integer as the oracle's (int64) cast)

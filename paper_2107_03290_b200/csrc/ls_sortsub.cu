@@ -674,7 +674,22 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(S - 1u);
         uint32_t code[WS_KPL];
-        if (g != g_lo && g != g_hi) {
+        if (task.w != 0u && g != g_lo && g != g_hi) {
+            // one leaf holds every key and p = its line value (k_classify's
+            // contained_leaf_warp: no routing, no clamp)
+            const double *q = a.M->leaf + 5 * (task.w - 1u);
+            const double la = __ldg(q), lc = __ldg(q + 1), lb = __ldg(q + 2);
+#pragma unroll
+            for (int k = 0; k < WS_KPL; k++) {
+                code[k] = BS_NONE;
+                if (32u * k + lane < np) {
+                    const double p = __fma_rn(la, __dsub_rn(xd<DT>(key[k]), lc), lb);
+                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t r = atomicAdd(&W.K[pos], 1u);
+                    code[k] = pos | (r << 16);
+                }
+            }
+        } else if (g != g_lo && g != g_hi) {
             // leaf of every key (O6 routing); a sub-bucket spans ~1/f^2 of the
             // CDF, so its keys almost always share one leaf, whose line is then
             // read once into registers instead of per key
