@@ -312,7 +312,8 @@ def run_ours(args):
     pristine = torch.empty(n, dtype=tdt, device=dev)
     plan.device(pristine)
     keys = torch.empty_like(pristine)
-    cfg = ls.config(flags=ls.LS_FLAG_PHASE_TIMING)
+    cfg = ls.config(flags=ls.LS_FLAG_PHASE_TIMING |
+                    (ls.LS_FLAG_PEER_SCATTER if multi and not args.no_peer_scatter else 0))
     dt = ls.dtype_code(pristine)
     if multi:
         comm = ls.Comm.from_torch_distributed() if world > 1 else ls.Comm(0, 1, ls.Comm.unique_id())
@@ -425,6 +426,24 @@ def run_ours(args):
         line["error"] = "output check failed (sortedness or multiset hash)"
     if multi:
         line["n_out_rank0"] = n_out
+        # per-rank device times (median over the timed steps) and the exchange:
+        # keys each rank sent to other ranks cross NVLink once (8 B each); the
+        # north_star roofline adds that NVLink term to the HBM one
+        med_ms = float(np.median(times)) if times else 0.0
+        remote = int(stats[-1].get("remote_keys", 0)) if stats else 0
+        if world > 1:
+            allv = [None] * world
+            dist.all_gather_object(allv, (med_ms, remote, int(stats[-1].get("peer_scatter", 0))))
+        else:
+            allv = [(med_ms, remote, int(stats[-1].get("peer_scatter", 0)) if stats else 0)]
+        nv_bytes = max(v[1] for v in allv) * 8
+        nv_peak = 900.0  # GB/s per direction per B200 (NVLink 5, nominal)
+        line["per_rank_ms"] = [round(v[0], 4) for v in allv]
+        line["peer_scatter"] = [v[2] for v in allv]
+        line["nvlink"] = {"bytes_per_rank_max": nv_bytes, "peak_gbs": nv_peak,
+                          "peak_source": "nominal NVLink 5 per direction (no measured figure)",
+                          "roofline_ms": nv_bytes / (nv_peak * 1e6),
+                          "achieved_gbs": (nv_bytes / 1e6 / max(v[0] for v in allv)) if allv and max(v[0] for v in allv) > 0 else None}
 
     # e2e: the same metric through the C ABI with HOST buffers -- ls_sort_host:
     # H2D of the pinned input, the sort, D2H of the sorted keys, all inside the
@@ -729,6 +748,8 @@ def main():
                     help="keys for the 1-core std::sort context baseline")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other 200M configs (dup budget) in the N=1 line")
+    ap.add_argument("--no-peer-scatter", action="store_true",
+                    help="multi-GPU: NCCL all-to-all instead of the fused peer-store scatter (SURVEY f1)")
     ap.add_argument("--force-multi", action="store_true",
                     help="run the ls_sort_multi path (config 5) even at world size 1")
     args = ap.parse_args()

@@ -47,6 +47,14 @@ typedef enum {
 /* flags */
 #define LS_FLAG_PHASE_TIMING 0x1ULL /* record CUDA events between phases (ls_stats.phase_ms) */
 #define LS_FLAG_VALIDATE_MODEL 0x2ULL /* ls_sort_with_model: reject unsafe models (default on) */
+#define LS_FLAG_PEER_SCATTER 0x8ULL /* ls_sort_multi: the destination scatter stores
+                                       every run straight into the destination rank's d_out (its
+                                       allocation mapped here with CUDA IPC: NVLink peer stores),
+                                       at this rank's slice of it; no send buffer, no NCCL
+                                       all-to-all (NCCL still carries the samples, the counts,
+                                       the handles and one closing all-reduce). d_out must be
+                                       device memory that CUDA IPC can export (cudaMalloc /
+                                       the PyTorch caching allocator). Same output. */
 #define LS_FLAG_FUSED_ROUND1 0x4ULL /* ls_sort: partition every level-0 bucket of 64K..~219K keys
                                        with one 8-CTA cluster (count and scatter of
                                        round 1 in one kernel, the bucket staged in shared memory,
@@ -103,6 +111,11 @@ typedef struct {
     uint64_t fused_buckets;             /* level-0 buckets partitioned cluster-resident (f2)  */
     uint64_t round0_exact;              /* 1: round 0 took the exact count pass (a sample-
                                            estimated bucket capacity did not hold)           */
+    uint64_t peer_scatter;              /* ls_sort_multi: 1 if LS_FLAG_PEER_SCATTER's fused peer
+                                           scatter ran (0: the NCCL all-to-all, also the collective
+                                           fallback when a buffer cannot be mapped)              */
+    uint64_t remote_keys;               /* ls_sort_multi: keys this rank sent to other ranks
+                                           (8 bytes each over NVLink)                           */
     float phase_ms[LS_NUM_PHASES];      /* with LS_FLAG_PHASE_TIMING                          */
 } ls_stats;
 
@@ -237,6 +250,22 @@ ls_status ls_multi_sample(const void *d_in, uint64_t n_in, int rank, ls_dtype dt
 ls_status ls_multi_route(const void *d_in, uint64_t n_in, int rank, int world,
                          const ls_tagged *h_splitters, ls_dtype dtype, void *d_send,
                          uint64_t *h_counts, void *d_ws, size_t ws_bytes, void *stream);
+/* SURVEY §8(f) f1, the fused destination scatter of LS_FLAG_PEER_SCATTER for
+ * ONE rank without a communicator: steps 3 + 5 with the given R-1 splitters,
+ * the scatter storing destination p's keys straight into h_dst[p] (a device
+ * pointer valid on this GPU: local memory, or a peer GPU's buffer mapped with
+ * CUDA IPC / peer access) from element h_dst_off[p] on, h_counts[p] of them
+ * (reported on the host), in no particular order inside. h_dst and h_dst_off
+ * are host arrays of `world` entries (8-byte-aligned pointers; unused when
+ * h_counts[p] == 0). Nothing is written before the counts are known; the
+ * caller sizes and places the slices (e.g. from every rank's counts, as
+ * ls_sort_multi does with ls_multi_plan). d_ws: ls_multi_workspace_bytes(n_in,
+ * 0, world, ...) bytes. Synchronous on `stream`. Errors: LS_E_INVALID,
+ * LS_E_WORKSPACE, LS_E_NAN (nothing written). */
+ls_status ls_multi_route_peer(const void *d_in, uint64_t n_in, int rank, int world,
+                              const ls_tagged *h_splitters, ls_dtype dtype, void *const *h_dst,
+                              const uint64_t *h_dst_off, uint64_t *h_counts, void *d_ws,
+                              size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ import ctypes as C
 
 from . import _lib
 from ._lib import (LS_E_CAPACITY, LS_E_CUDA, LS_E_INTERNAL, LS_E_INVALID, LS_E_NAN, LS_E_NCCL,
-                   LS_E_WORKSPACE, LS_F64, LS_FLAG_FUSED_ROUND1, LS_FLAG_PHASE_TIMING, LS_OK,
+                   LS_E_WORKSPACE, LS_F64, LS_FLAG_FUSED_ROUND1, LS_FLAG_PEER_SCATTER, LS_FLAG_PHASE_TIMING, LS_OK,
                    LS_U64, PHASES, Config,
                    Dumps, Leaf, Model, Stats, Tagged)
 
@@ -24,7 +24,7 @@ __all__ = [
     "multi_route", "Config", "Model",
     "Stats", "Dumps", "Tagged", "Leaf", "PHASES", "LS_F64", "LS_U64", "LS_OK", "LS_E_NAN",
     "LS_E_INVALID", "LS_E_WORKSPACE", "LS_E_CAPACITY", "LS_E_CUDA", "LS_E_NCCL", "LS_E_INTERNAL",
-    "LS_FLAG_PHASE_TIMING", "LS_FLAG_FUSED_ROUND1",
+    "LS_FLAG_PHASE_TIMING", "LS_FLAG_FUSED_ROUND1", "LS_FLAG_PEER_SCATTER", "multi_route_peer",
 ]
 
 
@@ -260,6 +260,27 @@ def multi_route(keys, rank: int, world: int, splitters, send, ws=None, stream=No
                               spl.ctypes.data if len(spl) else None, dt, _ptr(send),
                               counts.ctypes.data, _ptr(ws), ws.numel(), _stream(stream)),
            "ls_multi_route")
+    return counts
+
+
+def multi_route_peer(keys, rank: int, world: int, splitters, dsts, offsets, ws=None, stream=None):
+    """SURVEY f1's fused destination scatter for one rank without a
+    communicator: destination p's keys are stored into the device tensor
+    dsts[p] from element offsets[p] on; returns the destination counts."""
+    import numpy as np
+    import torch
+    dt = dtype_code(keys)
+    if ws is None:
+        ws = torch.empty(multi_workspace_bytes(keys.numel(), 0, world, dt), dtype=torch.uint8,
+                         device=keys.device)
+    spl = np.ascontiguousarray(splitters)
+    ptrs = (C.c_void_p * world)(*[_ptr(d) for d in dsts])
+    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    counts = np.zeros(world, np.uint64)
+    _check(lib.ls_multi_route_peer(_ptr(keys), keys.numel(), rank, world,
+                                   spl.ctypes.data if len(spl) else None, dt, ptrs,
+                                   offs.ctypes.data, counts.ctypes.data, _ptr(ws), ws.numel(),
+                                   _stream(stream)), "ls_multi_route_peer")
     return counts
 
 

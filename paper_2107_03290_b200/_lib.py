@@ -14,6 +14,7 @@ LS_MAX_LEAVES = 1024
 LS_FLAG_PHASE_TIMING = 0x1
 LS_FLAG_VALIDATE_MODEL = 0x2
 LS_FLAG_FUSED_ROUND1 = 0x4
+LS_FLAG_PEER_SCATTER = 0x8
 LS_MULTI_SAMPLE = 4096
 LS_UNIQUE_ID_BYTES = 128
 PHASES = ("fit", "count0", "scatter0", "count1", "scatter1", "classify", "bucketsort", "big")
@@ -24,7 +25,7 @@ EXPORTS = (
     "ls_train_rmi", "ls_sort", "ls_sort_with_model", "ls_sort_host", "ls_bucket_ids",
     "ls_comm_unique_id", "ls_comm_init", "ls_comm_destroy", "ls_multi_workspace_bytes",
     "ls_sort_multi", "ls_multi_splitters", "ls_multi_plan", "ls_multi_dest", "ls_multi_sample",
-    "ls_multi_route",
+    "ls_multi_route", "ls_multi_route_peer",
 )
 
 
@@ -50,7 +51,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "n", "h0_buckets", "h0_keys", "h1_subbuckets", "h1_keys", "small_subbuckets",
         "small_keys", "big_subbuckets", "big_keys", "max_group", "big_passes",
-        "kernel_launches", "fused_buckets", "round0_exact")] + [("phase_ms", C.c_float * len(PHASES))]
+        "kernel_launches", "fused_buckets", "round0_exact", "peer_scatter", "remote_keys")] + [("phase_ms", C.c_float * len(PHASES))]
 
     def as_dict(self) -> dict:
         d = {n: int(getattr(self, n)) for n, _ in self._fields_[:-1]}
@@ -99,6 +100,7 @@ def load() -> C.CDLL:
         "ls_multi_dest": (I, [P, I, U64, U32, U64]),
         "ls_multi_sample": (S, [P, U64, I, I, P, P]),
         "ls_multi_route": (S, [P, U64, I, I, P, I, P, P, P, C.c_size_t, P]),
+        "ls_multi_route_peer": (S, [P, U64, I, I, P, I, P, P, P, P, C.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -9,6 +9,7 @@
 // pass (the same machinery as a partition round, with R buckets), the shards
 // are exchanged with a grouped NCCL send/recv all-to-all over NVLink, and each
 // rank sorts what it received with the single-GPU path (local model refit).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -26,6 +27,14 @@
 struct ls_comm {
     ncclComm_t comm;
     int rank, world;
+    // LS_FLAG_PEER_SCATTER: the peers' d_out as mapped here (CUDA IPC), keyed
+    // by the exchanged (allocation handle, offset) so a reused buffer is
+    // opened once
+    struct Peer {
+        cudaIpcMemHandle_t h;
+        uint64_t off;
+        void *base;  // cudaIpcOpenMemHandle result (nullptr: not open)
+    } peer[64];
 };
 
 namespace ls {
@@ -94,6 +103,13 @@ struct MultiArgs {
     uint32_t *ticket;
 };
 
+// Per destination rank: its receive buffer as seen from this GPU and where
+// this rank's keys start in it.
+struct PeerDst {
+    uint64_t *ptr[MAX_WORLD];
+    uint64_t off[MAX_WORLD];
+};
+
 template <int DT>
 struct DestBucket {
     const Tagged *spl;
@@ -159,6 +175,49 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_dest_scatter(MultiArgs a) {
     tile_partition(S.tp, a.in, a.send, beg, end, a.n, S.base, R, bf, phase);
 }
 
+// the destination scatter fused with the exchange. Bucket p
+// = destination rank p; its runs are stored straight into rank p's receive
+// buffer (pdst[p], another GPU's HBM mapped through CUDA IPC: NVLink peer
+// stores) at this rank's slice of it, so there is no send buffer and no NCCL
+// all-to-all (-16 B/key of HBM traffic on each side), and the transfer
+// overlaps the partition work tile by tile.
+struct PeerSmem {
+    TpSmem tp;
+    uint32_t base[LS_MAX_FANOUT];
+    Tagged spl[MAX_WORLD];
+    uint64_t *pdst[MAX_WORLD];
+};
+
+template <int DT>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_dest_scatter_peer(MultiArgs a, PeerDst pd) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PeerSmem &S = *reinterpret_cast<PeerSmem *>(smem_raw);
+    const int tid = threadIdx.x, R = a.world;
+    const uint64_t u = blockIdx.x;
+    if (tid < R - 1) S.spl[tid] = a.spl[tid];
+    if (tid < R) {
+        S.base[tid] = (uint32_t)pd.off[tid] + a.offs[u * R + tid];
+        S.pdst[tid] = pd.ptr[tid];
+    }
+    tp_init(S.tp);
+    const uint64_t beg = u * MULTI_UNIT, end = umin64(a.n, beg + MULTI_UNIT);
+    const DestBucket<DT> bf{S.spl, R, a.rank};
+    uint32_t phase = 0;
+    tile_partition<false, false, false, DestBucket<DT>, TP_THREADS, TP_KPT, TpBids, false, true>(
+        S.tp, a.in, nullptr, beg, end, a.n, S.base, R, bf, phase, nullptr, nullptr, nullptr, nullptr, S.pdst);
+}
+
+static void launch_dest_scatter_peer(const MultiArgs &a, const PeerDst &pd, int dt, cudaStream_t st) {
+    const size_t sm = sizeof(PeerSmem);
+    if (dt == DT_F64) {
+        cudaFuncSetAttribute(k_dest_scatter_peer<DT_F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_dest_scatter_peer<DT_F64><<<a.U, TP_THREADS, sm, st>>>(a, pd);
+    } else {
+        cudaFuncSetAttribute(k_dest_scatter_peer<DT_U64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_dest_scatter_peer<DT_U64><<<a.U, TP_THREADS, sm, st>>>(a, pd);
+    }
+}
+
 static bool tagged_lt(const ls_tagged &x, const ls_tagged &y) {
     if (x.ord != y.ord) return x.ord < y.ord;
     if (x.rank != y.rank) return x.rank < y.rank;
@@ -168,8 +227,16 @@ static bool tagged_lt(const ls_tagged &x, const ls_tagged &y) {
 static size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
 struct MultiLayout {
-    size_t send, samp, gath, spl, lb, offs, counts, allcounts, sdispl, ticket, local, total;
+    size_t send, samp, gath, spl, lb, offs, counts, allcounts, sdispl, ticket, xchg, local, total;
     uint32_t U;
+};
+
+// LS_FLAG_PEER_SCATTER: what every rank publishes about its d_out
+struct PeerXchg {
+    cudaIpcMemHandle_t h;  // of the allocation that holds d_out
+    uint64_t off;          // d_out - allocation base
+    uint64_t ok;           // 1: the handle could be exported
+    uint64_t pad[6];
 };
 
 static MultiLayout multi_layout(uint64_t n_in, uint64_t out_cap, int R, const ls_config &cfg) {
@@ -190,9 +257,29 @@ static MultiLayout multi_layout(uint64_t n_in, uint64_t out_cap, int R, const ls
     l.offs = take((size_t)l.U * R * 4);
     l.allcounts = take((size_t)(R + 2) * R * 8);
     l.sdispl = take((size_t)R * 8);
+    l.xchg = take((size_t)(R + 1) * sizeof(PeerXchg));  // (+1: the barrier word)
     l.local = al(off);
     l.total = l.local + workspace_bytes(out_cap > 1 ? out_cap : 2, cfg);
     return l;
+}
+
+// Base of the allocation that holds p (the driver's cuMemGetAddressRange,
+// reached through the runtime: libls does not link libcuda).
+static cudaError_t alloc_base(const void *p, uint64_t *base) {
+    typedef CUresult (*RangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static RangeFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !f) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        fn = (RangeFn)f;
+    }
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    *base = (uint64_t)b;
+    return cudaSuccess;
 }
 
 }  // namespace ls
@@ -289,6 +376,8 @@ ls_status ls_comm_init(const uint8_t id[LS_UNIQUE_ID_BYTES], int rank, int world
 
 void ls_comm_destroy(ls_comm *comm) {
     if (!comm) return;
+    for (int p = 0; p < MAX_WORLD; p++)
+        if (comm->peer[p].base) cudaIpcCloseMemHandle(comm->peer[p].base);
     ncclCommDestroy(comm->comm);
     delete comm;
 }
@@ -378,6 +467,70 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     *n_out = nout;
     if (any_nan) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
     if (any_cap) { set_error("out_cap smaller than the received key count on some rank"); return LS_E_CAPACITY; }
+    // LS_FLAG_PEER_SCATTER: every rank's d_out mapped here, or,
+    // if any rank cannot export / map its buffer, the send-buffer path below
+    // on every rank (the decision is collective: all-gathered flags and one
+    // all-reduce of the mapping results)
+    bool peer = (cfg.flags & LS_FLAG_PEER_SCATTER) != 0;
+    PeerDst pd;
+    memset(&pd, 0, sizeof pd);
+    if (peer && R > 1) {
+        PeerXchg mine;
+        memset(&mine, 0, sizeof mine);
+        uint64_t base = 0;
+        if (alloc_base(d_out, &base) == cudaSuccess && cudaIpcGetMemHandle(&mine.h, (void *)base) == cudaSuccess) {
+            mine.off = (uint64_t)(uintptr_t)d_out - base;
+            mine.ok = 1;
+        }
+        cudaGetLastError();  // (a failed export is not an error: the collective fallback)
+        unsigned char *xb = w + l.xchg;
+        CUDA_CHECK(cudaMemcpyAsync(xb + (size_t)R * sizeof(PeerXchg), &mine, sizeof mine, cudaMemcpyHostToDevice, st));
+        NCCL_CHECK(ncclAllGather(xb + (size_t)R * sizeof(PeerXchg), xb, sizeof(PeerXchg), ncclUint8, comm->comm, st));
+        std::vector<PeerXchg> xs(R);
+        CUDA_CHECK(cudaMemcpyAsync(xs.data(), xb, (size_t)R * sizeof(PeerXchg), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int p = 0; p < R; p++) peer &= xs[p].ok == 1;
+        if (peer) {
+            uint64_t mapped = 1;
+            for (int p = 0; p < R; p++) {
+                if (p == me) continue;
+                ls_comm::Peer &pe = comm->peer[p];
+                if (!pe.base || memcmp(&pe.h, &xs[p].h, sizeof pe.h) != 0) {
+                    if (pe.base) cudaIpcCloseMemHandle(pe.base);
+                    pe.base = nullptr;
+                    if (cudaIpcOpenMemHandle(&pe.base, xs[p].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                        pe.base = nullptr;
+                        mapped = 0;
+                        cudaGetLastError();
+                        continue;
+                    }
+                    pe.h = xs[p].h;
+                }
+                pe.off = xs[p].off;
+                pd.ptr[p] = (uint64_t *)((unsigned char *)pe.base + pe.off);
+            }
+            CUDA_CHECK(cudaMemcpyAsync(xb, &mapped, 8, cudaMemcpyHostToDevice, st));
+            NCCL_CHECK(ncclAllReduce(xb, xb, 1, ncclUint64, ncclMin, comm->comm, st));
+            CUDA_CHECK(cudaMemcpyAsync(&mapped, xb, 8, cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            peer = mapped == 1;
+        }
+    }
+    if (peer) {
+        // 5'+6'. the destination scatter stores each run straight into its
+        // destination's d_out at this rank's slice (the ranks before it come
+        // first: ls_multi_plan's receive order); one all-reduce then orders
+        // every rank's stores before any local sort
+        pd.ptr[me] = (uint64_t *)d_out;
+        for (int p = 0; p < R; p++) {
+            uint64_t o = 0;
+            for (int q = 0; q < me; q++) o += mat[(size_t)q * R + p];
+            pd.off[p] = o;
+        }
+        if (n_in) launch_dest_scatter_peer(a, pd, dt, st);
+        CUDA_CHECK(cudaGetLastError());
+        NCCL_CHECK(ncclAllReduce(w + l.xchg, w + l.xchg, 1, ncclUint64, ncclMax, comm->comm, st));
+    } else {
     // 5. scatter by destination into the send buffer
     CUDA_CHECK(cudaMemcpyAsync(w + l.sdispl, sd.data(), (size_t)R * 8, cudaMemcpyHostToDevice, st));
     if (n_in) {
@@ -393,19 +546,26 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     CUDA_CHECK(cudaGetLastError());
     // 6. all-to-all over NVLink
     const uint64_t *send = a.send;
-    uint64_t *out = (uint64_t *)d_out;
     NCCL_CHECK(ncclGroupStart());
     for (int p = 0; p < R; p++) {
         const uint64_t sc = mat[(size_t)me * R + p];
         if (sc) NCCL_CHECK(ncclSend(send + sd[p], sc, ncclUint64, p, comm->comm, st));
-        if (rcnt[p]) NCCL_CHECK(ncclRecv(out + rd[p], rcnt[p], ncclUint64, p, comm->comm, st));
+        if (rcnt[p]) NCCL_CHECK(ncclRecv((uint64_t *)d_out + rd[p], rcnt[p], ncclUint64, p, comm->comm, st));
     }
     NCCL_CHECK(ncclGroupEnd());
+    }
     // 7. local LearnedSort 2.0 (fresh model on the received keys)
     Pending pend;
-    rc = enqueue_sort(out, nout, dtype, &cfg, nullptr, w + l.local, ws_bytes - l.local, st, stats, nullptr, &pend);
+    rc = enqueue_sort((uint64_t *)d_out, nout, dtype, &cfg, nullptr, w + l.local, ws_bytes - l.local, st, stats, nullptr, &pend);
     if (rc != LS_OK) return rc;
-    return finish_sort(&pend, st, stats);
+    rc = finish_sort(&pend, st, stats);
+    if (stats) {
+        stats->peer_scatter = peer ? 1u : 0u;
+        uint64_t rk = 0;
+        for (int p = 0; p < R; p++) rk += p == me ? 0 : mat[(size_t)me * R + p];
+        stats->remote_keys = rk;
+    }
+    return rc;
 }
 
 ls_status ls_multi_sample(const void *d_in, uint64_t n_in, int rank, ls_dtype dtype,
@@ -485,6 +645,68 @@ ls_status ls_multi_route(const void *d_in, uint64_t n_in, int rank, int world,
             k_dest_scatter<DT_U64><<<l.U, TP_THREADS, sm, st>>>(a);
         }
     }
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    return LS_OK;
+}
+
+ls_status ls_multi_route_peer(const void *d_in, uint64_t n_in, int rank, int world,
+                              const ls_tagged *h_splitters, ls_dtype dtype, void *const *h_dst,
+                              const uint64_t *h_dst_off, uint64_t *h_counts, void *d_ws,
+                              size_t ws_bytes, void *stream) {
+    if (world < 1 || world > MAX_WORLD || rank < 0 || rank >= world || !h_counts || !d_ws ||
+        (world > 1 && !h_splitters) || (n_in && (!d_in || !h_dst || !h_dst_off))) {
+        set_error("bad arguments");
+        return LS_E_INVALID;
+    }
+    if (dtype != LS_F64 && dtype != LS_U64) { set_error("bad dtype"); return LS_E_INVALID; }
+    if (n_in >= (1ull << 32)) { set_error("n must be < 2^32"); return LS_E_INVALID; }
+    if (((uintptr_t)d_in & 15) || ((uintptr_t)d_ws & 255)) {
+        set_error("keys must be 16-byte aligned and the workspace 256-byte aligned");
+        return LS_E_INVALID;
+    }
+    ls_config cfg;
+    ls_config_default(&cfg);
+    const int R = world;
+    const MultiLayout l = multi_layout(n_in, 0, R, cfg);
+    if (ws_bytes < l.local) { set_error("workspace too small"); return LS_E_WORKSPACE; }
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned char *w = (unsigned char *)d_ws;
+    const int dt = (int)dtype;
+    if (R > 1) CUDA_CHECK(cudaMemcpyAsync(w + l.spl, h_splitters, (size_t)(R - 1) * sizeof(Tagged), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemsetAsync(w + l.ticket, 0, l.send - l.ticket, st));
+    MultiArgs a;
+    a.in = (const uint64_t *)d_in;
+    a.send = nullptr;
+    a.n = n_in;
+    a.rank = (uint32_t)rank;
+    a.world = R;
+    a.U = l.U;
+    a.spl = (const Tagged *)(w + l.spl);
+    a.lb = (unsigned long long *)(w + l.lb);
+    a.offs = (uint32_t *)(w + l.offs);
+    a.counts = (unsigned long long *)(w + l.counts);
+    a.sdispl = (const unsigned long long *)(w + l.sdispl);
+    a.ticket = (uint32_t *)(w + l.ticket);
+    if (n_in) {
+        if (dt == DT_F64) k_dest_count<DT_F64><<<l.U, 512, 0, st>>>(a);
+        else k_dest_count<DT_U64><<<l.U, 512, 0, st>>>(a);
+    }
+    std::vector<unsigned long long> row((size_t)R + 1);
+    CUDA_CHECK(cudaMemcpyAsync(row.data(), a.counts, row.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (row[R]) { set_error("NaN key in input (S:214)"); return LS_E_NAN; }
+    PeerDst pd;
+    memset(&pd, 0, sizeof pd);
+    for (int p = 0; p < R; p++) {
+        h_counts[p] = row[p];
+        if (n_in) {
+            if (row[p] && (!h_dst[p] || ((uintptr_t)h_dst[p] & 7))) { set_error("bad destination pointer"); return LS_E_INVALID; }
+            pd.ptr[p] = (uint64_t *)h_dst[p];
+            pd.off[p] = h_dst_off[p];
+        }
+    }
+    if (n_in) launch_dest_scatter_peer(a, pd, dt, st);
     CUDA_CHECK(cudaGetLastError());
     CUDA_CHECK(cudaStreamSynchronize(st));
     return LS_OK;

@@ -99,15 +99,19 @@ __device__ __forceinline__ void tp_issue(SM &S, int slot, const uint64_t *src, u
 // BIDS: the bucket of key i is bid[i] (precomputed by the count pass, staged
 // by the bulk engine next to the keys); bf is not called.
 // RESERVE: base is unused; runs are reserved through *rs (TpReserve).
+// PEER: bucket b's runs go to pdst[b] + cursor (pdst: shared memory, one
+// pointer per bucket -- a destination rank's receive buffer, possibly another
+// GPU's memory mapped through CUDA IPC: the stores cross NVLink); dst unused.
 template <bool SKIP = false, bool BIDS = false, bool ISSUED = false, class BF, int NT = TP_THREADS,
-          int KPT = TP_KPT, class SB = TpBids, bool RESERVE = false>
+          int KPT = TP_KPT, class SB = TpBids, bool RESERVE = false, bool PEER = false>
 __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64_t *__restrict__ src,
                                                uint64_t *__restrict__ dst, uint64_t beg,
                                                uint64_t end, uint64_t len, uint32_t *base,
                                                int nb, const BF &bf, uint32_t &phase,
                                                const uint16_t *bid = nullptr, SB *sb = nullptr,
                                                unsigned long long *prof = nullptr,
-                                               const TpReserve *rs = nullptr) {
+                                               const TpReserve *rs = nullptr,
+                                               uint64_t *const *pdst = nullptr) {
     constexpr int TILE = NT * KPT;
     constexpr int BPT = (LS_MAX_FANOUT + NT - 1) / NT;  // buckets per thread in the scan
     long long tq = clock64();
@@ -265,6 +269,8 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
                 if (RESERVE) {
                     const uint32_t q = d[k] + (uint32_t)idx;
                     if (idx < tm && q < rs->lim) dst[q] = v[k];
+                } else if (PEER) {
+                    if (idx < tm) pdst[b[k]][d[k] + (uint32_t)idx] = v[k];
                 } else if (idx < tm) {
                     dst[d[k] + (uint32_t)idx] = v[k];
                 }

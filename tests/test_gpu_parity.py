@@ -447,6 +447,81 @@ def test_multi_route_world_gt1(world, dist):
     assert np.array_equal(bits(np.concatenate(out)), bits(O.sort(h)[0]))
 
 
+@pytest.mark.parametrize("world,dist", [(2, "normal"), (3, "zipf"), (8, "cfg5mix"), (5, "telemetry"),
+                                        (4, "twodups")])
+def test_multi_route_peer_world_gt1(world, dist):
+    """SURVEY f1 (LS_FLAG_PEER_SCATTER's fused scatter) for R > 1 virtual ranks
+    on one GPU: each rank's destination scatter stores its runs straight into
+    the R receive buffers (separate allocations standing for the peers' d_out)
+    at its own slice (after the lower ranks', as ls_sort_multi places them).
+    Checked: the counts equal the send-buffer path's, every slice holds exactly
+    the keys the host rule sends there, no slice spills into another (the
+    buffers start filled with a sentinel and every key is accounted for), the
+    split is balanced (R = 8: within 10 % of n/R), and sorting the receive
+    buffers one by one reproduces the oracle's global order."""
+    rng = np.random.default_rng(world + 100)
+    n = 1_500_007
+    keys = gen(dist, n, 37)
+    h = to_np(keys)
+    cuts = np.concatenate([[0], np.sort(rng.choice(np.arange(1, n), world - 1, replace=False)), [n]])
+    shards = [keys[cuts[r]:cuts[r + 1]].clone() for r in range(world)]
+    gathered = np.concatenate([ls.multi_sample(sh, r) for r, sh in enumerate(shards)])
+    spl = ls.multi_splitters(gathered.copy(), world)
+    sends, mat = [], []
+    for r, sh in enumerate(shards):
+        send = torch.empty_like(sh)
+        mat.append(ls.multi_route(sh, r, world, spl, send))
+        sends.append(to_np(send))
+    mat = np.stack(mat).astype(np.int64)          # mat[r][p]: keys rank r sends to p
+    sizes = mat.sum(0)
+    assert sizes.sum() == n
+    assert sizes.max() <= 1.10 * n / world, f"imbalanced split: {sizes}"
+    sent_bits = np.uint64(0x7ff4dead0000beef)    # (a NaN pattern: never a generated key)
+    recv = [torch.full((int(sizes[p]) + 8,), 0, dtype=torch.int64, device=DEV) for p in range(world)]
+    for t in recv:
+        t.fill_(int(sent_bits.astype(np.int64)))
+    recv = [t.view(keys.dtype) for t in recv]
+    for r, sh in enumerate(shards):
+        off = mat[:r].sum(0).astype(np.uint64)
+        got = ls.multi_route_peer(sh, r, world, spl, recv, off)
+        assert np.array_equal(got.astype(np.int64), mat[r])
+    for p in range(world):
+        rp = to_np(recv[p])
+        assert np.all(bits(rp[sizes[p]:]) == sent_bits)      # nothing past the slices
+        o = 0
+        for r in range(world):
+            sd = np.concatenate([[0], np.cumsum(mat[r])])
+            want = sends[r][sd[p]:sd[p + 1]]
+            part = rp[o:o + mat[r][p]]
+            assert np.array_equal(np.sort(ord_np(part)), np.sort(ord_np(want)))
+            o += mat[r][p]
+    out = []
+    for p in range(world):
+        t = recv[p][:sizes[p]].clone()
+        if t.numel():
+            ls.ls_sort(t)
+        out.append(to_np(t))
+    assert np.array_equal(bits(np.concatenate(out)), bits(O.sort(h)[0]))
+
+
+def test_sort_multi_single_rank_peer_scatter():
+    """ls_sort_multi with LS_FLAG_PEER_SCATTER on a one-rank communicator: the
+    fused scatter writes straight into d_out (the rank's own slice), one NCCL
+    all-reduce, the local sort -- the oracle's output."""
+    comm = ls.Comm(0, 1, ls.Comm.unique_id())
+    try:
+        cfg = ls.config(flags=ls.LS_FLAG_PEER_SCATTER)
+        for dist, n in (("cfg5mix", 2_000_000), ("twodups", 300_001), ("normal", 1)):
+            keys = gen(dist, n, 1001)
+            h = to_np(keys)
+            out = torch.empty(n + 1000, dtype=keys.dtype, device=DEV)
+            n_out, st = ls.ls_sort_multi(comm, keys, out, cfg=cfg)
+            assert n_out == n and st["peer_scatter"] == 1
+            assert np.array_equal(bits(to_np(out[:n_out])), bits(O.sort(h)[0]))
+    finally:
+        comm.close()
+
+
 # -------------------------------------------------- large big sub-buckets --
 
 def _clusters(dtype, seed):
