@@ -308,7 +308,7 @@ constexpr uint32_t CS_MAX = 4096;  // SMALL sub-buckets of WS_MAX+1..CS_MAX keys
 //   257..1024 one 128-thread CTA (8 keys per thread); 1025..2048 one
 //   128-thread CTA (16 per thread); 2049..T_small one 256-thread CTA;
 //   > T_small the exact big path.
-enum { SC_TRIVIAL = 0, SC_WINDOW, SC_WARP, SC_CTAL, SC_CTAM, SC_CTA, SC_BIG };
+enum { SC_TRIVIAL = 0, SC_WINDOW, SC_WARP, SC_CTAL, SC_CTAM, SC_CTA, SC_BIG, SC_FUSED };  // (SC_FUSED: sorted by k_round1)
 __host__ __device__ __forceinline__ int size_class(uint32_t np, uint32_t T_small) {
     if (np <= 1) return SC_TRIVIAL;
     if (np > T_small) return SC_BIG;

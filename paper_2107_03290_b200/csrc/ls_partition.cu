@@ -560,7 +560,10 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     const uint32_t st = j < f ? (uint32_t)bbeg + s[j] : 0u;
     // SMALL sub-buckets of <= WS_MAX keys become warp tasks (compacted per
     // block: one global atomic per level-0 bucket)
-    const int sc = j < f ? size_class(c, a.T_small) : SC_TRIVIAL;
+    // (a bucket of the cluster-resident round 1 has its warp-sized
+    // sub-buckets sorted there already: k_round1's P5)
+    const int sc0 = j < f ? size_class(c, a.T_small) : SC_TRIVIAL;
+    const int sc = (sc0 == SC_WARP && a.fused[b]) ? SC_FUSED : sc0;
     // warp / CTA sorts become task lists (compacted per block: one global
     // atomic per level-0 bucket and class)
     {

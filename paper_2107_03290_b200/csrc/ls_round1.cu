@@ -38,6 +38,7 @@
 
 #include "ls_common.cuh"
 #include "ls_launch.h"
+#include "ls_wstask.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -71,8 +72,13 @@ __global__ void __cluster_dims__(FR_CL, 1, 1) __launch_bounds__(FR_THREADS, 1) k
     const double *leaf = a.M->leaf;
     // the only level-0 buckets that can hold keys outside [xmin, xmax] (they
     // are clamped onto xmin / xmax): elsewhere the root clamp is skipped
-    const uint32_t b_lo = sub_bucket_at(R.xmin, R, leaf, a.F, a.F2, f) / (uint32_t)f;
-    const uint32_t b_hi = sub_bucket_at(R.xmax, R, leaf, a.F, a.F2, f) / (uint32_t)f;
+    const uint32_t g_lo = sub_bucket_at(R.xmin, R, leaf, a.F, a.F2, f);
+    const uint32_t g_hi = sub_bucket_at(R.xmax, R, leaf, a.F, a.F2, f);
+    const uint32_t b_lo = g_lo / (uint32_t)f, b_hi = g_hi / (uint32_t)f;
+    // P5 state: per-warp statistics and the warp sort's adaptive flags
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t r_maxg = 0, wst[4] = {0u, 0u, 0u, 0u};
+    bool early_h1 = false;
     if (tid == 0) mbar_init(&S.mbar, 1);
     uint32_t phase = 0;
     const bool prof = (a.dbg & 8192u) && tid == 0;
@@ -221,7 +227,6 @@ __global__ void __cluster_dims__(FR_CL, 1, 1) __launch_bounds__(FR_THREADS, 1) k
         // P4: one run per sub-bucket (~n'/FR_CL keys) to its place in A, one
         // warp per sub-bucket (runs 8x longer than k_scatter1's per-tile runs)
         {
-            const int lane = tid & 31, warp = tid >> 5;
             uint64_t *dst = a.A + bbeg;
             for (int j = warp; j < f; j += FR_THREADS / 32) {
                 const uint32_t cnt = S.hist[j], lo = S.cur[j] - cnt, d = S.dst[j];
@@ -229,8 +234,36 @@ __global__ void __cluster_dims__(FR_CL, 1, 1) __launch_bounds__(FR_THREADS, 1) k
             }
         }
         mark(5);
+        // P5 (f2, second half): the bucket's SMALL sub-buckets of <= WS_MAX keys
+        // (Alg. 2's counting sort + touch-up, ws_task) sorted by the cluster's
+        // 256 warps right after the scatter, while its lines are in L2; each
+        // warp's slice lives in the (consumed) region; k_classify lists no warp
+        // task for a fused bucket. Starts and sizes: rank 0's P2 table (DSMEM).
+        cl.sync();  // (C) every CTA's runs are in A
+        {
+            WsSlice *SL = reinterpret_cast<WsSlice *>(S.region);
+            for (int j = (int)rank * (FR_THREADS / 32) + warp; j < f; j += FR_CL * (FR_THREADS / 32)) {
+                const uint32_t s0j = *cl.map_shared_rank(&S.dst[j], 0);
+                const uint32_t s1j = j + 1 < f ? *cl.map_shared_rank(&S.dst[j + 1], 0) : nb;
+                const uint32_t c = s1j - s0j;
+                if (size_class(c, a.T_small) != SC_WARP) continue;  // (warp-uniform)
+                const uint32_t g = b * (uint32_t)f + (uint32_t)j;
+                const uint32_t wl = contained_leaf_warp(leaf, R.Lm1 + 1, g, g, a.rcpF2, lane);
+                ws_task<DT>(a, R, g_lo, g_hi, SL[warp], wst, r_maxg, early_h1,
+                            make_uint4((uint32_t)bbeg + s0j, c, g, wl), lane);
+            }
+        }
+        mark(6);
+    }
+    if (lane == 0) {
+        if (wst[0]) atomicAdd(&a.ctl->stat[ST_SMALLS], (unsigned long long)wst[0]);
+        if (wst[1]) atomicAdd(&a.ctl->stat[ST_SMALLK], (unsigned long long)wst[1]);
+        if (wst[2]) atomicAdd(&a.ctl->stat[ST_H1S], (unsigned long long)wst[2]);
+        if (wst[3]) atomicAdd(&a.ctl->stat[ST_H1K], (unsigned long long)wst[3]);
+        if (r_maxg > 1) atomicMax(&a.ctl->stat[ST_MAXGRP], (unsigned long long)r_maxg);
     }
 }
+static_assert(sizeof(WsSlice) * (FR_THREADS / 32) <= sizeof(uint64_t) * FR_Q, "P5 warp slices fit the region");
 
 // Active clusters of k_round1 per device (-1: not probed, 0: unavailable).
 // cudaFuncSetAttribute and the cluster occupancy are per device, so the probe

@@ -148,6 +148,14 @@ def test_sort_bit_exact_1e7(dist):
     check_sort(gen(dist, 10_000_000, 11))
 
 
+@pytest.mark.parametrize("dist,seed", [("twodups", 13), ("twodups", 5), ("zipf", 13), ("zipf", 5)])
+def test_sort_bit_exact_3e6_dups(dist, seed):
+    """Regression: at 3M duplicate-heavy keys the warp sort meets several
+    all-equal collision groups > 8 keys in one sub-bucket (skipping one must
+    not end the sub-bucket's touch-up)."""
+    check_sort(gen(dist, 3_000_000, seed))
+
+
 # ------------------------------------------ cluster-resident round 1 (f2) --
 
 FUSED = dict(flags=ls.LS_FLAG_FUSED_ROUND1)
@@ -167,12 +175,17 @@ def test_fused_round1_bit_exact(dist, monkeypatch):
     assert st["fused_buckets"] > 0
     st2, _ = check_sort(keys)
     assert st2["fused_buckets"] == 0
+    # P5 (the in-bucket sort inside k_round1) accounts for the same sub-buckets
+    for k in ("small_subbuckets", "small_keys", "h1_subbuckets", "h1_keys", "big_keys"):
+        assert st[k] == st2[k], k
 
 
 def test_fused_round1_default_threshold():
-    """At 70M keys the level-0 buckets (~70K keys) take the cluster path."""
+    """At 70M keys the level-0 buckets (~70K keys) take the cluster path, and
+    their ~70-key sub-buckets are sorted inside it (P5)."""
     st, _ = check_sort(gen("normal", 70_000_000, 17), cfg=ls.config(**FUSED))
     assert st["fused_buckets"] >= 990
+    assert st["small_keys"] > 60_000_000
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 31, 99, 100, 101, 2047, 2048, 2049, 4097, 8191, 8192,
