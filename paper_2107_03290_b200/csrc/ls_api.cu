@@ -42,7 +42,7 @@ struct Layout {
     int f, L;
     uint32_t C0, C1, U0, U1max, T_small, T_tile, ntiles, big_cap;
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
-        offs1, hist1, start1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
+        hist1, start1, cur1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
         cap0, bsrc, cur0, shist0,
         lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist,
         border;
@@ -107,8 +107,8 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.start0 = take((size_t)(l.f + 1) * 8);
     l.ustart = take((size_t)(l.f + 1) * 4);
     l.offs0 = take((size_t)l.U0 * l.f * 4);
-    l.offs1 = take((size_t)l.U1max * l.f * 4);
     l.start1 = take(ff * 4);
+    l.cur1 = take(ff * 4);
     l.wlist = take((size_t)l.ntiles * 16);
     // B: the scratch copy of the partition rounds. Round 0 by reservation
     // leaves each level-0 bucket a sample-estimated capacity (k_cap0), so B
@@ -178,9 +178,9 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.unit1_start = (uint32_t *)(w + l.ustart);
     a.lb0 = (unsigned long long *)(w + l.lb0);
     a.offs0 = (uint32_t *)(w + l.offs0);
-    a.offs1 = (uint32_t *)(w + l.offs1);
     a.hist1 = (uint32_t *)(w + l.hist1);
     a.start1 = (uint32_t *)(w + l.start1);
+    a.cur1 = (uint32_t *)(w + l.cur1);
     a.tile_first = (uint32_t *)(w + l.tfirst);
     a.tile_last = (uint32_t *)(w + l.tlast);
     a.wlist = (uint4 *)(w + l.wlist);

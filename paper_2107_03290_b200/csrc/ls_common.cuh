@@ -389,9 +389,9 @@ struct Args {
     uint64_t Bcap;                    // keys B holds (>= n)
     uint32_t force_exact0;            // host: always take the exact count pass
     uint32_t *offs0;                  // [U0*f]
-    uint32_t *offs1;                  // [U1max*f]
     uint32_t *hist1;                  // [f*f]
     uint32_t *start1;                 // [f*f]
+    uint32_t *cur1;                   // [f*f] round-1 write cursors (k_scatter1 reserves runs on them)
     uint32_t *tile_first, *tile_last; // [ntiles]
     uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
     uint16_t *bid;                    // [n + 16] bucket id of each key, count -> scatter pass

@@ -19,6 +19,8 @@
 #include "ls_tile.cuh"
 #include "ls_tilepart.cuh"
 
+#include <cstdlib>
+
 namespace ls {
 
 // ----------------------------------------------------------------- init ----
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0r(Args a) {
         }
         return bs.get<DT>(key);
     };
-    const TpReserve rs{a.cur0, a.cap0, a.bsrc, &a.ctl->exact0, (uint32_t)a.Bcap};
+    const TpReserve rs{a.cur0, a.cap0, a.bsrc, &a.ctl->exact0, (uint32_t)a.Bcap, nullptr};
     uint32_t phase = 0;
     tile_partition<false, false, false, decltype(bf), TP_THREADS, TP_KPT, TpBids, true>(
         S.tp, a.A, a.B, t0 * TP_TILE, umin64(a.n, t1 * TP_TILE), a.n, nullptr, a.f, bf, phase, nullptr,
@@ -472,26 +474,28 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     for (int j = tid; j < f; j += bd) {
         const uint32_t c = hist[j];
         if (c) atomicAdd(&a.hist1[(uint64_t)b * f + j], c);
-        a.offs1[(uint64_t)u * f + j] = c;  // per-unit counts; k_classify scans them per bucket
     }
 }
 
-struct Scatter1Smem {
-    TpSmem tp;
-    alignas(16) TpBids sbid;
-    uint32_t base[LS_MAX_FANOUT];
+template <int NT>
+struct Scatter1SmemT {
+    TpSmemT<NT, TP_KPT> tp;
+    alignas(16) TpBidsT<NT * TP_KPT> sbid;
     uint32_t ustart[LS_MAX_FANOUT + 1];
 };
+typedef Scatter1SmemT<TP_THREADS> Scatter1Smem;
+constexpr int SC1_NT2 = 512;  // two CTAs per SM, 4K-key tiles (LS_SC1_NT=512)
 
 static_assert(sizeof(Scatter0Smem) <= MAX_SMEM_OPTIN, "scatter0 shared memory");
 static_assert(sizeof(Scatter0rSmem) + 64 <= MAX_SMEM_OPTIN, "scatter0r shared memory");
 static_assert(sizeof(Scatter1Smem) <= MAX_SMEM_OPTIN, "scatter1 shared memory");
+static_assert(2 * (sizeof(Scatter1SmemT<SC1_NT2>) + 1024) <= 233472, "scatter1 (512) two per SM");
 
-template <int DT>
-__global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
+template <int DT, int NT>
+__global__ void __launch_bounds__(NT, TP_THREADS / NT) k_scatter1(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Scatter1Smem &S = *reinterpret_cast<Scatter1Smem *>(smem_raw);
-    const int f = a.f, tid = threadIdx.x, bd = TP_THREADS;
+    Scatter1SmemT<NT> &S = *reinterpret_cast<Scatter1SmemT<NT> *>(smem_raw);
+    const int f = a.f, tid = threadIdx.x, bd = NT;
     const uint32_t u = blockIdx.x;
     if (u >= a.ctl->U1 || a.ctl->status) return;
     for (int b = tid; b <= f; b += bd) S.ustart[b] = a.unit1_start[b];
@@ -513,16 +517,22 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1(Args a) {
         for (uint64_t i = beg + tid; i < end; i += bd) Ab[i] = v;
         return;
     }
-    // the first tiles are staged right away; meanwhile the cursors: sub-bucket
-    // starts (k_classify's start1) + this unit's offsets inside them
+    // the first tiles are staged right away. Every tile reserves its run in
+    // sub-bucket g with one atomicAdd on g's cursor (k_classify: cur1 = start1;
+    // the counts are exact, so nothing overflows): the runs of one sub-bucket
+    // are written front to back in time by whichever CTAs hold its keys, so
+    // its L2 sectors fill up before they are evicted. (Per-unit regions,
+    // start1 + the unit's offset, left each unit's boundary sectors partly
+    // written for a whole CTA lifetime: ~0.36 GB of DRAM read-modify-write
+    // per 200M keys.)
     if (tid == 0) tp_issue_first(S.tp, a.B, beg, end, a.Bcap, a.bid, &S.sbid);
-    for (int j = tid; j < f; j += bd)
-        S.base[j] = a.start1[(uint64_t)b * f + j] + a.offs1[(uint64_t)u * f + j];
     __syncthreads();
     uint32_t phase = 0;
     const NoBucket bf{};
-    tile_partition<false, true, true>(S.tp, a.B, a.A, beg, end, a.Bcap, S.base, f, bf, phase, a.bid, &S.sbid,
-                                      (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr);
+    const TpReserve rs{nullptr, nullptr, nullptr, nullptr, (uint32_t)a.n, a.cur1 + (uint64_t)b * f};
+    tile_partition<false, true, true, NoBucket, NT, TP_KPT, TpBidsT<NT * TP_KPT>, true>(
+        S.tp, a.B, a.A, beg, end, a.Bcap, nullptr, f, bf, phase, a.bid, &S.sbid,
+        (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr, &rs);
 }
 
 // ------------------------------------------------------------- classify ----
@@ -601,21 +611,8 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         }
     }
     if (j < f) {
-        // offs1: per-unit counts (k_count1) -> this unit's offset inside sub-bucket j
-        const uint32_t u0 = a.unit1_start[b], u1 = a.unit1_start[b + 1];
-        uint32_t run = 0;
-        for (uint32_t u = u0; u < u1; u += 8) {  // 8 independent loads in flight
-            uint32_t cnt[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                cnt[q] = u + q < u1 ? a.offs1[(uint64_t)(u + q) * f + j] : 0u;
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                if (u + q < u1) a.offs1[(uint64_t)(u + q) * f + j] = run;
-                run += cnt[q];
-            }
-        }
         a.start1[g] = st;
+        a.cur1[g] = st;
         if (sc == SC_TRIVIAL) {
             if (a.dH1) a.dH1[g] = 1;
         } else if (sc == SC_WINDOW) {  // tiny sub-buckets: block windows
@@ -738,9 +735,16 @@ void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     else { set_smem(k_count1<DT_U64>, sm); k_count1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
 }
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
+    static const bool nt2 = [] { const char *e = getenv("LS_SC1_NT"); return e && atoi(e) == SC1_NT2; }();
+    if (nt2) {
+        const size_t sm = sizeof(Scatter1SmemT<SC1_NT2>);
+        if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64, SC1_NT2>, sm); k_scatter1<DT_F64, SC1_NT2><<<a.U1max, SC1_NT2, sm, st>>>(a); }
+        else { set_smem(k_scatter1<DT_U64, SC1_NT2>, sm); k_scatter1<DT_U64, SC1_NT2><<<a.U1max, SC1_NT2, sm, st>>>(a); }
+        return;
+    }
     const size_t sm = sizeof(Scatter1Smem);
-    if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64>, sm); k_scatter1<DT_F64><<<a.U1max, TP_THREADS, sm, st>>>(a); }
-    else { set_smem(k_scatter1<DT_U64>, sm); k_scatter1<DT_U64><<<a.U1max, TP_THREADS, sm, st>>>(a); }
+    if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64, TP_THREADS>, sm); k_scatter1<DT_F64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
+    else { set_smem(k_scatter1<DT_U64, TP_THREADS>, sm); k_scatter1<DT_U64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
 }
 void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st) {
     (void)dS_B1;

@@ -54,11 +54,14 @@ typedef TpBidsT<TP_TILE> TpBids;
 // b owns dst[bsrc[b], bsrc[b] + cap[b]). A run that would pass cap[b] is not
 // written and raises *ovf (the caller then redoes the round exactly). lim =
 // an index no valid run reaches (stores at or beyond it are dropped).
+// cur32 != nullptr: exact 32-bit cursors (absolute destination indices,
+// k_scatter1): no capacities, nothing overflows; cur, cap, bsrc, ovf unused.
 struct TpReserve {
     unsigned long long *cur;
     const unsigned long long *cap, *bsrc;
     uint32_t *ovf;
     uint32_t lim;
+    uint32_t *cur32;
 };
 
 constexpr uint32_t TP_SKIP = 0xffffu;  // bucket id of keys that are not moved (SKIP mode)
@@ -132,7 +135,7 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
     for (int b = tid; b < nb; b += NT) S.cnt[b] = 0;
     // RESERVE: this thread's buckets' capacities and regions, once
     unsigned long long rcap[RESERVE ? BPT : 1], rsrc[RESERVE ? BPT : 1];
-    if (RESERVE) {
+    if (RESERVE && !rs->cur32) {
 #pragma unroll
         for (int j = 0; j < BPT; j++) {
             const int b = BPT * tid + j;
@@ -191,7 +194,9 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
 #pragma unroll
             for (int j = 0; j < BPT; j++) {
                 const int b = BPT * tid + j;
-                rsv[j] = cb[j] ? atomicAdd(&rs->cur[b], (unsigned long long)cb[j]) : 0ull;
+                rsv[j] = !cb[j] ? 0ull
+                         : rs->cur32 ? (unsigned long long)atomicAdd(&rs->cur32[b], cb[j])
+                                     : atomicAdd(&rs->cur[b], (unsigned long long)cb[j]);
             }
         }
         const uint32_t incl = warp_incl_scan(c);
@@ -238,7 +243,9 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
                 const int b = BPT * tid + j;
                 if (cb[j]) {
                     uint32_t d;
-                    if (rsv[j] + cb[j] <= rcap[j]) {
+                    if (rs->cur32) {
+                        d = (uint32_t)rsv[j] - e;
+                    } else if (rsv[j] + cb[j] <= rcap[j]) {
                         d = (uint32_t)(rsrc[j] + rsv[j]) - e;
                     } else {  // over capacity: dropped (the round is redone exactly)
                         d = rs->lim;

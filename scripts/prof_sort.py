@@ -16,6 +16,7 @@ ap.add_argument("--n", type=int, default=50_000_000)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--flags", type=lambda x: int(x, 0), default=0, help="extra LS_FLAG_* bits")
+ap.add_argument("--big", type=int, default=4096, help="big_threshold of the config")
 a = ap.parse_args()
 plan = datagen.Plan(a.dist, a.n, a.seed)
 tdt = torch.float64 if plan.dtype == np.float64 else torch.uint64
@@ -25,7 +26,7 @@ keys = torch.empty_like(src)
 ws = ls.workspace(a.n, ls.dtype_code(src))
 for r in range(a.reps):
     keys.copy_(src)
-    st = ls.ls_sort(keys, ws=ws, cfg=ls.config(flags=ls.LS_FLAG_PHASE_TIMING | a.flags))
+    st = ls.ls_sort(keys, ws=ws, cfg=ls.config(flags=ls.LS_FLAG_PHASE_TIMING | a.flags, big_threshold=a.big))
     print(r, {k: round(v, 3) for k, v in st["phase_ms"].items()}, st["small_keys"], st["h1_keys"],
           st["big_keys"])
 torch.cuda.synchronize()
