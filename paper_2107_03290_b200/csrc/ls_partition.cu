@@ -265,19 +265,36 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
 // 5 standard deviations), the scatter reserves every tile's run in its bucket
 // with one atomicAdd, and the count pass (k_count0) runs only if a bucket
 // overflowed or the capacities did not fit B. S_B = the final cursors (exact).
+// The sample's level-0 histogram: b0 search tables staged in shared memory,
+// 8 independent keys per thread (the lookups of one key are a dependent
+// chain; a global-memory version with one key at a time was latency-bound:
+// 45 us for 2M keys at 200M).
+struct SampHistSmem {
+    B0Smem b0;
+    uint32_t h[LS_MAX_FANOUT];
+};
+constexpr int SH_THREADS = 512;
 template <int DT>
-__global__ void __launch_bounds__(256) k_samp_hist0(Args a, uint64_t m) {
-    __shared__ uint32_t h[LS_MAX_FANOUT];
-    const int f = a.f;
-    for (int b = threadIdx.x; b < f; b += blockDim.x) h[b] = 0;
+__global__ void __launch_bounds__(SH_THREADS, 2) k_samp_hist0(Args a, uint64_t m) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SampHistSmem &S = *reinterpret_cast<SampHistSmem *>(smem_raw);
+    const int f = a.f, tid = threadIdx.x;
+    for (int b = tid; b < f; b += SH_THREADS) S.h[b] = 0;
+    const B0Search bs = load_b0_search(S.b0, a.M);
     __syncthreads();
-    const DevModel *M = a.M;
-    const B0Search bs{M->xmin, M->xmax, M->cell_scale, M->nthr, M->thr, M->cell, M->sub};
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(&h[bs.get<DT>(a.S[i])], 1u);
+    constexpr int U = 8;
+    const uint64_t gs = (uint64_t)gridDim.x * SH_THREADS * U;
+    for (uint64_t i = (uint64_t)blockIdx.x * SH_THREADS * U + tid; i < m; i += gs) {
+        uint64_t k[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) k[q] = i + q * SH_THREADS < m ? a.S[i + q * SH_THREADS] : 0ull;
+#pragma unroll
+        for (int q = 0; q < U; q++)
+            if (i + q * SH_THREADS < m) atomicAdd(&S.h[bs.get<DT>(k[q])], 1u);
+    }
     __syncthreads();
-    for (int b = threadIdx.x; b < f; b += blockDim.x)
-        if (h[b]) atomicAdd(&a.shist0[b], h[b]);
+    for (int b = tid; b < f; b += SH_THREADS)
+        if (S.h[b]) atomicAdd(&a.shist0[b], S.h[b]);
 }
 
 __global__ void __launch_bounds__(1024) k_cap0(Args a, uint64_t m) {
@@ -705,9 +722,14 @@ void launch_plan0(const Args &a, uint64_t *dS_B, int reserved, cudaStream_t st) 
     k_plan0<<<1, 1024, 0, st>>>(a, dS_B, reserved);
 }
 void launch_cap0(const Args &a, uint64_t m, int dtype, cudaStream_t st) {
-    const unsigned g = (unsigned)umin64((m + 1023) / 1024, 148);
-    if (dtype == DT_F64) k_samp_hist0<DT_F64><<<g ? g : 1, 256, 0, st>>>(a, m);
-    else k_samp_hist0<DT_U64><<<g ? g : 1, 256, 0, st>>>(a, m);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t per = (uint64_t)SH_THREADS * 8;
+    const unsigned g = (unsigned)umin64((m + per - 1) / per, 2ull * (uint64_t)sms);
+    const size_t sm = sizeof(SampHistSmem);
+    if (dtype == DT_F64) { set_smem(k_samp_hist0<DT_F64>, sm); k_samp_hist0<DT_F64><<<g ? g : 1, SH_THREADS, sm, st>>>(a, m); }
+    else { set_smem(k_samp_hist0<DT_U64>, sm); k_samp_hist0<DT_U64><<<g ? g : 1, SH_THREADS, sm, st>>>(a, m); }
     k_cap0<<<1, 1024, 0, st>>>(a, m);
 }
 void launch_scatter0r(const Args &a, int dtype, cudaStream_t st) {

@@ -4,7 +4,7 @@ make -j8 > gpurun_out/make.log 2>&1; echo "make rc=$?"
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 cat gpurun_out/bench.json
-BENCH="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+BENCH="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-configs"
 $BENCH > gpurun_out/bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $BENCH > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
