@@ -19,8 +19,6 @@
 #include "ls_tile.cuh"
 #include "ls_tilepart.cuh"
 
-#include <cstdlib>
-
 namespace ls {
 
 // ----------------------------------------------------------------- init ----
@@ -501,12 +499,12 @@ struct Scatter1SmemT {
     uint32_t ustart[LS_MAX_FANOUT + 1];
 };
 typedef Scatter1SmemT<TP_THREADS> Scatter1Smem;
-constexpr int SC1_NT2 = 512;  // two CTAs per SM, 4K-key tiles (LS_SC1_NT=512)
+// (measured: two 512-thread CTAs per SM with 4K-key tiles, 1.40 ms against
+// 1.03 ms for one 1024-thread CTA with 8K-key tiles at 200M Normal)
 
 static_assert(sizeof(Scatter0Smem) <= MAX_SMEM_OPTIN, "scatter0 shared memory");
 static_assert(sizeof(Scatter0rSmem) + 64 <= MAX_SMEM_OPTIN, "scatter0r shared memory");
 static_assert(sizeof(Scatter1Smem) <= MAX_SMEM_OPTIN, "scatter1 shared memory");
-static_assert(2 * (sizeof(Scatter1SmemT<SC1_NT2>) + 1024) <= 233472, "scatter1 (512) two per SM");
 
 template <int DT, int NT>
 __global__ void __launch_bounds__(NT, TP_THREADS / NT) k_scatter1(Args a) {
@@ -757,13 +755,6 @@ void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     else { set_smem(k_count1<DT_U64>, sm); k_count1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
 }
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
-    static const bool nt2 = [] { const char *e = getenv("LS_SC1_NT"); return e && atoi(e) == SC1_NT2; }();
-    if (nt2) {
-        const size_t sm = sizeof(Scatter1SmemT<SC1_NT2>);
-        if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64, SC1_NT2>, sm); k_scatter1<DT_F64, SC1_NT2><<<a.U1max, SC1_NT2, sm, st>>>(a); }
-        else { set_smem(k_scatter1<DT_U64, SC1_NT2>, sm); k_scatter1<DT_U64, SC1_NT2><<<a.U1max, SC1_NT2, sm, st>>>(a); }
-        return;
-    }
     const size_t sm = sizeof(Scatter1Smem);
     if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64, TP_THREADS>, sm); k_scatter1<DT_F64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
     else { set_smem(k_scatter1<DT_U64, TP_THREADS>, sm); k_scatter1<DT_U64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
