@@ -151,17 +151,21 @@ ls_status ls_train_rmi(const void *d_sample, uint64_t m, ls_dtype dtype, const l
                        ls_model *out, void *d_ws, size_t ws_bytes, void *stream);
 
 /* Sort n keys in place (Alg. 2): strided sample + fit, level-0
- * partition (count -> decoupled-lookback offsets -> scatter), level-1
- * segmented partition, homogeneous-bucket skip, model counting sort with
- * collision-group touch-up, exact big-bucket path. dumps/stats may be NULL.
+ * partition (one scatter pass reserving runs in per-bucket capacities taken
+ * from the sample; the exact count -> decoupled-lookback -> scatter passes
+ * only when a capacity does not hold), level-1 segmented partition (count,
+ * then a scatter reserving runs on one cursor per sub-bucket), homogeneous-
+ * bucket skip, model counting sort with collision-group touch-up, exact
+ * big-bucket path. dumps/stats may be NULL.
  * d_keys must be 16-byte aligned and d_ws 256-byte aligned (cudaMalloc /
  * torch allocations are; an odd-offset slice is not): LS_E_INVALID otherwise,
  * for every entry point that takes device keys and a workspace.
  * Launch sequence: every decision inside it is taken on the device, so the
  * second call with the same (d_keys, n, dtype, cfg, d_ws, device) captures it
  * into a CUDA Graph and later calls replay it with one launch (kept in a
- * 16-entry process-wide cache; not used with dumps, LS_FLAG_PHASE_TIMING or
- * ls_sort_with_model). Environment: LS_GRAPH=0 launches directly; LS_GRAPH=2
+ * 16-entry process-wide cache; not used with dumps or ls_sort_with_model;
+ * with LS_FLAG_PHASE_TIMING the phase events are event-record nodes of the
+ * graph). Environment: LS_GRAPH=0 launches directly; LS_GRAPH=2
  * turns a failed capture into LS_E_CUDA instead of a direct launch. */
 ls_status ls_sort(void *d_keys, uint64_t n, ls_dtype dtype, const ls_config *cfg, void *d_ws,
                   size_t ws_bytes, void *stream, ls_stats *stats, const ls_dumps *dumps);

@@ -11,6 +11,21 @@
 
 namespace ls {
 
+// One sample key: a single 8-byte word per 800 bytes of input, so the load
+// asks L2 for a 64-byte fill (LS_SAMPLE_L2: 0 = plain streaming load)
+#ifndef LS_SAMPLE_L2
+#define LS_SAMPLE_L2 64
+#endif
+__device__ __forceinline__ uint64_t ld_sample(const uint64_t *p) {
+#if LS_SAMPLE_L2 == 64
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+
 template <int DT>
 __global__ void __launch_bounds__(256) k_sample_minmax(const uint64_t *__restrict__ src,
                                                        uint64_t stride, uint64_t m,
@@ -24,7 +39,7 @@ __global__ void __launch_bounds__(256) k_sample_minmax(const uint64_t *__restric
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t k = k0 + u * gs;
-            b[u] = k < m ? __ldcs(src + k * stride) : 0ull;
+            b[u] = k < m ? ld_sample(src + k * stride) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -238,22 +253,91 @@ __global__ void __launch_bounds__(256) k_b0_thresholds(DevModel *M, int f) {
     }
 }
 
+// Smallest o in [omin, omax] with pred(o) (pred monotone false ... true; the
+// caller has checked pred(omax)), found from a guess o0 in [omin, omax]:
+// gallop away from o0 to bracket the first true point, then bisect the
+// bracket. The result is the plain bisection's for any guess; a guess a few
+// ulps off (the grid boundaries below) needs a handful of evaluations instead
+// of 64.
+template <class P>
+__device__ __forceinline__ unsigned long long first_true_from(const P &pred, unsigned long long omin,
+                                                              unsigned long long omax, unsigned long long o0) {
+    unsigned long long lo, hi;
+    if (pred(o0)) {
+        hi = o0;
+        lo = omin;
+        for (unsigned long long d = 1; hi > omin;) {
+            const unsigned long long c = hi - omin > d ? hi - d : omin;
+            if (!pred(c)) { lo = c + 1; break; }
+            hi = c;
+            if (c == omin) { lo = omin; break; }
+            d = d < (1ull << 62) ? 2 * d : d;
+        }
+    } else {
+        lo = o0 + 1;
+        hi = omax;
+        for (unsigned long long d = 1;;) {
+            const unsigned long long c = omax - lo > d ? lo + d : omax;
+            if (pred(c)) { hi = c; break; }
+            lo = c + 1;  // (c < omax: pred(omax) holds)
+            d = d < (1ull << 62) ? 2 * d : d;
+        }
+    }
+    while (lo < hi) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        if (pred(mid)) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// The ord of the key nearest the double x, clamped into [omin, omax] (a
+// starting guess only).
+template <int DT>
+__device__ __forceinline__ unsigned long long guess_ord(double x, unsigned long long omin, unsigned long long omax) {
+    if (!(x == x) || x - x != 0.0) return omin;  // (NaN / inf: no guess)
+    unsigned long long o;
+    if (DT == DT_F64) o = to_ord<DT>((uint64_t)__double_as_longlong(x + 0.0));
+    else o = x <= 0.0 ? 0ull : x >= 18446744073709549568.0 ? ~0ull : (unsigned long long)x;
+    return o < omin ? omin : o > omax ? omax : o;
+}
+
+// #thresholds < s and <= o_hi (thr in shared memory, V of them)
+__device__ __forceinline__ void thr_range(const unsigned long long *thr, uint32_t V, unsigned long long s,
+                                          unsigned long long o_hi, uint32_t &off, uint32_t &end) {
+    off = 0;
+    end = 0;
+    for (uint32_t lo = 0, n = V; n > 0;) {
+        const uint32_t h = n >> 1;
+        if (thr[lo + h] < s) { lo += h + 1; n -= h + 1; } else n = h;
+        off = lo;
+    }
+    for (uint32_t lo = 0, n = V; n > 0;) {
+        const uint32_t h = n >> 1;
+        if (thr[lo + h] <= o_hi) { lo += h + 1; n -= h + 1; } else n = h;
+        end = lo;
+    }
+}
+
 // one thread per grid cell (16K cells: parallel enough for plain bisection)
 template <int DT>
 __global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
+    __shared__ unsigned long long thr[LS_MAX_FANOUT];
+    const uint32_t V = M->nthr;
+    for (uint32_t i = threadIdx.x; i < V; i += blockDim.x) thr[i] = M->thr[i];
+    __syncthreads();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= B0_CELLS) return;
     const double xmin = M->xmin, xmax = M->xmax, cs = M->cell_scale;
     unsigned long long omin, omax;
     ord_domain<DT>(omin, omax);
+    // first ord of grid cell >= target: bisection started at the cell's
+    // nominal left edge xmin + target / cs
     auto first_ge = [&](int target, bool &none) {
-        unsigned long long lo = omin, hi = omax;
-        none = b0_cell<DT>(from_ord<DT>(hi), xmin, xmax, cs) < target;
-        while (lo < hi) {
-            const unsigned long long mid = lo + (hi - lo) / 2;
-            if (b0_cell<DT>(from_ord<DT>(mid), xmin, xmax, cs) >= target) hi = mid; else lo = mid + 1;
-        }
-        return lo;
+        auto pred = [&](unsigned long long o) { return b0_cell<DT>(from_ord<DT>(o), xmin, xmax, cs) >= target; };
+        none = !pred(omax);
+        if (none) return omax;
+        const double xg = cs > 0.0 ? __dadd_rn(xmin, __ddiv_rn((double)target, cs)) : xmin;
+        return first_true_from(pred, omin, omax, guess_ord<DT>(xg, omin, omax));
     };
     bool none0, none1;
     const unsigned long long s = first_ge(c, none0);
@@ -261,18 +345,8 @@ __global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
     uint32_t entry = 0;
     if (!none0 && (none1 || e > s)) {  // cell c owns ords [s, o_hi]
         const unsigned long long o_hi = none1 ? omax : e - 1;
-        const uint32_t V = M->nthr;
-        uint32_t off = 0, end = 0;  // #thr < s, #thr <= o_hi
-        for (uint32_t lo = 0, n = V; n > 0;) {
-            const uint32_t h = n >> 1;
-            if (M->thr[lo + h] < s) { lo += h + 1; n -= h + 1; } else n = h;
-            off = lo;
-        }
-        for (uint32_t lo = 0, n = V; n > 0;) {
-            const uint32_t h = n >> 1;
-            if (M->thr[lo + h] <= o_hi) { lo += h + 1; n -= h + 1; } else n = h;
-            end = lo;
-        }
+        uint32_t off, end;  // #thr < s, #thr <= o_hi
+        thr_range(thr, V, s, o_hi, off, end);
         const uint32_t cnt = end - off;
         entry = off | ((cnt < B0_REFINED ? cnt : B0_SAT) << 10);
         if (cnt >= B0_SUBMIN) {  // dense cell: refined by k_b0_sub if a sub-grid is left
@@ -291,21 +365,25 @@ __global__ void __launch_bounds__(256) k_b0_cells(DevModel *M) {
 // B0_SAT above). One thread per (k, s).
 template <int DT>
 __global__ void __launch_bounds__(256) k_b0_sub(DevModel *M) {
+    const uint32_t nsub = min(M->nsub, (uint32_t)B0_NSUB);
+    if (blockIdx.x * blockDim.x / B0_SUB >= nsub) return;  // (whole block past the sub-grids)
+    __shared__ unsigned long long thr[LS_MAX_FANOUT];
+    const uint32_t V = M->nthr;
+    for (uint32_t i = threadIdx.x; i < V; i += blockDim.x) thr[i] = M->thr[i];
+    __syncthreads();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t k = (uint32_t)t / B0_SUB, sidx = (uint32_t)t % B0_SUB;
-    if (k >= min(M->nsub, (uint32_t)B0_NSUB)) return;
+    if (k >= nsub) return;
     const int fc = (int)M->sub_cell[k] * B0_SUB + (int)sidx;  // fine index of this sub-cell
     const double xmin = M->xmin, cs = M->cell_scale;
     unsigned long long omin, omax;
     ord_domain<DT>(omin, omax);
     auto first_ge = [&](int target, bool &none) {
-        unsigned long long lo = omin, hi = omax;
-        none = b0_fine<DT>(from_ord<DT>(hi), xmin, cs) < target;
-        while (lo < hi) {
-            const unsigned long long mid = lo + (hi - lo) / 2;
-            if (b0_fine<DT>(from_ord<DT>(mid), xmin, cs) >= target) hi = mid; else lo = mid + 1;
-        }
-        return lo;
+        auto pred = [&](unsigned long long o) { return b0_fine<DT>(from_ord<DT>(o), xmin, cs) >= target; };
+        none = !pred(omax);
+        if (none) return omax;
+        const double xg = cs > 0.0 ? __dadd_rn(xmin, __ddiv_rn((double)target, __dmul_rn(cs, (double)B0_SUB))) : xmin;
+        return first_true_from(pred, omin, omax, guess_ord<DT>(xg, omin, omax));
     };
     bool none0, none1;
     const unsigned long long s = first_ge(fc, none0);
@@ -313,18 +391,8 @@ __global__ void __launch_bounds__(256) k_b0_sub(DevModel *M) {
     uint32_t entry = 0;
     if (!none0 && (none1 || e > s)) {  // sub-cell owns ords [s, o_hi]
         const unsigned long long o_hi = none1 ? omax : e - 1;
-        const uint32_t V = M->nthr;
-        uint32_t off = 0, end = 0;  // #thr < s, #thr <= o_hi
-        for (uint32_t lo = 0, n = V; n > 0;) {
-            const uint32_t h = n >> 1;
-            if (M->thr[lo + h] < s) { lo += h + 1; n -= h + 1; } else n = h;
-            off = lo;
-        }
-        for (uint32_t lo = 0, n = V; n > 0;) {
-            const uint32_t h = n >> 1;
-            if (M->thr[lo + h] <= o_hi) { lo += h + 1; n -= h + 1; } else n = h;
-            end = lo;
-        }
+        uint32_t off, end;  // #thr < s, #thr <= o_hi
+        thr_range(thr, V, s, o_hi, off, end);
         const uint32_t cnt = end - off;
         entry = off | ((cnt < B0_REFINED ? cnt : B0_SAT) << 10);
     }
