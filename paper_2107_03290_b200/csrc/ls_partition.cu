@@ -387,13 +387,30 @@ __device__ __forceinline__ int find_bucket(const uint32_t *ustart, int f, uint32
 template <int DT>
 constexpr bool C1_NARROW = DT == DT_F64;
 constexpr int C1_LEAVES = 64;
+// p of a key of a bucket whose keys all route to one leaf (its line in
+// registers): predict() without the routing and the leaf loads
+template <int DT>
+struct OneLeaf {
+    double la, lc, lb, llo, lhi;
+    __device__ __forceinline__ double operator()(uint64_t key) const {
+        const double y = __fma_rn(la, __dsub_rn(xd<DT>(key), lc), lb);
+        return __dadd_rn(clampd(y, llo, lhi), 0.0);
+    }
+};
 template <int DT, bool INNER>
+struct LeafTable {
+    const Root &R;
+    const double *leaf;
+    __device__ __forceinline__ double operator()(uint64_t key) const { return predict_c<DT, INNER>(key, R, leaf); }
+};
+
+template <class PRED>
 __device__ __forceinline__ void count1_range(const Args &a, int b, uint64_t beg, uint64_t end, uint64_t k0,
-                                             const Root &R, const double *leaf, uint32_t *hist, bool &diff) {
+                                             const PRED &pred, uint32_t *hist, bool &diff) {
     const int tid = threadIdx.x, bd = blockDim.x, f = a.f;
     auto one = [&](uint64_t key) -> uint32_t {
         diff |= key != k0;
-        const double p = predict_c<DT, INNER>(key, R, leaf);  // keys of one bucket: 1-2 leaves, broadcast
+        const double p = pred(key);  // keys of one bucket: 1-2 leaves, broadcast
         const uint32_t b1 = bucket1(p, a.F2, f, (uint32_t)b);
         atomicAdd(&hist[b1], 1u);
         return b1;
@@ -446,10 +463,11 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     // so only leaves llo..lhi are staged (typically one or two, not all L)
     const Root R = load_root(a.M);
     const double *leaf = a.M->leaf;
+    int llo, lhi;
     {
         double xc;
-        int llo = b > 0 ? root_leaf<DT>(from_ord<DT>(a.M->thr[b - 1]), R, xc) : 0;
-        int lhi = (uint32_t)b < a.M->nthr ? root_leaf<DT>(from_ord<DT>(a.M->thr[b] - 1ull), R, xc) : R.Lm1;
+        llo = b > 0 ? root_leaf<DT>(from_ord<DT>(a.M->thr[b - 1]), R, xc) : 0;
+        lhi = (uint32_t)b < a.M->nthr ? root_leaf<DT>(from_ord<DT>(a.M->thr[b] - 1ull), R, xc) : R.Lm1;
         if (C1_NARROW<DT>) {
             if (llo >= 0 && llo <= lhi && lhi - llo < C1_LEAVES) {
                 for (int i = tid; i < 5 * (lhi - llo + 1); i += bd) s_leaf[i] = a.M->leaf[5 * llo + i];
@@ -479,10 +497,17 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     // (they are clamped onto xmin / xmax): elsewhere the root clamp is skipped
     const uint32_t b_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, f) / (uint32_t)f;
     const uint32_t b_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, f) / (uint32_t)f;
-    if ((uint32_t)b != b_lo && (uint32_t)b != b_hi)
-        count1_range<DT, true>(a, b, beg, end, k0, R, leaf, hist, diff);
-    else
-        count1_range<DT, false>(a, b, beg, end, k0, R, leaf, hist, diff);
+    if ((uint32_t)b != b_lo && (uint32_t)b != b_hi) {
+        if (llo == lhi) {  // every key of the bucket routes to leaf llo
+            const double *q = a.M->leaf + 5 * llo;
+            const OneLeaf<DT> pred{__ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(q + 3), __ldg(q + 4)};
+            count1_range(a, b, beg, end, k0, pred, hist, diff);
+        } else {  // (two leaves with both lines in registers measured slower: 0.43 vs 0.40 ms)
+            count1_range(a, b, beg, end, k0, LeafTable<DT, true>{R, leaf}, hist, diff);
+        }
+    } else {
+        count1_range(a, b, beg, end, k0, LeafTable<DT, false>{R, leaf}, hist, diff);
+    }
     // bmin0[b] = ord of the bucket's first key, bmax0[b] != 0 iff two keys differ
     if (__syncthreads_or(diff) && tid == 0) a.bmax0[b] = 1ull;
     if (tid == 0 && beg < end) a.bmin0[b] = to_ord<DT>(k0);

@@ -10,5 +10,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo "ncu launches rc=$?"
 P="python scripts/prof_sort.py --dist normal --n 200000000 --reps 2"
 $P > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_count0|k_scatter0|k_count1|k_scatter1|k_warpsort|k_bucketsort" -s 6 -c 6 -o gpurun_out/prof_full $P > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_count0|k_scatter0|k_count1|k_scatter1|k_warpsort|k_bucketsort" -s 7 -c 8 -o gpurun_out/prof_full $P > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
