@@ -216,8 +216,9 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
 
 /* Host-side planning steps of ls_sort_multi, exported so the exchange logic can
  * be exercised without GPUs (gloo tests). Entries are (ord, rank, index)
- * triples. ls_multi_splitters: sorts `count` gathered sample entries and
- * writes the R-1 entries at ranks floor(k*count/R), k=1..R-1. ls_multi_plan:
+ * triples. ls_multi_splitters: writes the R-1 entries of ranks floor(k*v/R),
+ * k=1..R-1, in the lexicographic order of the v non-sentinel entries among the
+ * `count` gathered sample entries (reordering h_entries). ls_multi_plan:
  * from the R x R count matrix (row = source rank) computes, for `rank`, the
  * send displacements, the receive counts/displacements and n_out. */
 typedef struct {
@@ -248,7 +249,7 @@ int ls_multi_dest(const ls_tagged *h_splitters, int world, uint64_t ord, uint32_
  *   ls_multi_workspace_bytes(n_in, 0, world, ...) bytes. Synchronous on
  *   `stream`. Errors: LS_E_INVALID (bad sizes / world), LS_E_WORKSPACE,
  *   LS_E_NAN (NaN key; d_send untouched). */
-#define LS_MULTI_SAMPLE 4096
+#define LS_MULTI_SAMPLE 16384
 ls_status ls_multi_sample(const void *d_in, uint64_t n_in, int rank, ls_dtype dtype,
                           ls_tagged *d_samples, void *stream);
 ls_status ls_multi_route(const void *d_in, uint64_t n_in, int rank, int world,

@@ -15,7 +15,7 @@ LS_FLAG_PHASE_TIMING = 0x1
 LS_FLAG_VALIDATE_MODEL = 0x2
 LS_FLAG_FUSED_ROUND1 = 0x4
 LS_FLAG_PEER_SCATTER = 0x8
-LS_MULTI_SAMPLE = 4096
+LS_MULTI_SAMPLE = 16384
 LS_UNIQUE_ID_BYTES = 128
 PHASES = ("fit", "count0", "scatter0", "count1", "scatter1", "classify", "bucketsort", "big")
 

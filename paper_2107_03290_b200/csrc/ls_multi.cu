@@ -310,9 +310,21 @@ ls_status ls_multi_splitters(ls_tagged *h_entries, uint64_t count, int world, ls
         set_error("bad arguments");
         return LS_E_INVALID;
     }
-    std::sort(h_entries, h_entries + count, tagged_lt);
-    uint64_t valid = 0;  // sentinel entries (rank 0xffffffff) sort last
-    while (valid < count && h_entries[valid].rank != 0xffffffffu) valid++;
+    // sentinel entries (rank 0xffffffff) go last; then only the R-1 order
+    // statistics are needed: successive nth_element calls, each on the part
+    // right of the previous one (O(count log R) instead of a full sort)
+    ls_tagged *mid = std::partition(h_entries, h_entries + count,
+                                    [](const ls_tagged &e) { return e.rank != 0xffffffffu; });
+    const uint64_t valid = (uint64_t)(mid - h_entries);
+    {
+        uint64_t from = 0;
+        for (int k = 1; k < world && valid; k++) {
+            const uint64_t q = (uint64_t)k * valid / (uint64_t)world;
+            if (q < from) continue;  // (same rank as the previous splitter)
+            std::nth_element(h_entries + from, h_entries + q, h_entries + valid, tagged_lt);
+            from = q + 1;
+        }
+    }
     for (int k = 1; k < world; k++) {
         if (valid == 0) {
             h_splitters[k - 1].ord = ~0ull;

@@ -22,7 +22,7 @@ torch = pytest.importorskip("torch")
 import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
-SPLIT_K = 4096  # sample entries per rank (ls_multi.cu SPLIT_K)
+SPLIT_K = 16384  # sample entries per rank (ls_multi.cu SPLIT_K = LS_MULTI_SAMPLE)
 TAGGED = np.dtype([("ord", "<u8"), ("rank", "<u4"), ("pad", "<u4"), ("index", "<u8")])
 
 
