@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libls.so")
+SO_PATH = os.environ.get("LS_LIBPATH") or os.path.join(_HERE, "libls.so")  # (override: A/B runs)
 
 LS_F64, LS_U64 = 0, 1
 LS_OK, LS_E_INVALID, LS_E_NAN, LS_E_WORKSPACE, LS_E_CAPACITY, LS_E_CUDA, LS_E_NCCL, LS_E_INTERNAL = range(8)
