@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 PHASE_OF = {"k_count0": "count0", "k_scatter0": "scatter0", "k_scatter0r": "scatter0", "k_count1": "count1",
-            "k_scatter1": "scatter1", "k_warpsort": "bucketsort", "k_bucketsort": "bucketsort",
+            "k_scatter1": "scatter1", "k_warpsort": "bucketsort", "k_bucketsort": "bucketsort", "k_ctasort": "bucketsort",
             "k_big": "big"}
 
 
