@@ -126,11 +126,17 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
         }
     };
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t ntl = (end - beg + TILE - 1) / TILE;
+    // tiles start at even key positions (tbase + i * TILE, tbase = beg rounded
+    // down to even), so every staged tile is 16-byte aligned in its ring slot
+    // and the rank phase reads key pairs (and id pairs) with one vector load;
+    // the first tile's key at tbase < beg (when beg is odd) is not ours
+    static_assert(KPT % 2 == 0, "tile_partition reads key pairs");
+    const uint64_t tbase = beg & ~1ull;
+    const uint64_t ntl = end > beg ? (end - tbase + TILE - 1) / TILE : 0;
     if (ntl == 0) return;
     if (!ISSUED && tid == 0)  // (ISSUED: the caller has staged the first tiles, tp_issue_first)
         for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && j < ntl; j++)
-            tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)j, src, beg + j * TILE, umin64(end, beg + (j + 1) * TILE), len,
+            tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)j, src, tbase + j * TILE, umin64(end, tbase + (j + 1) * TILE), len,
                      BIDS ? bid : nullptr, sb);
     for (int b = tid; b < nb; b += NT) S.cnt[b] = 0;
     // RESERVE: this thread's buckets' capacities and regions, once
@@ -146,24 +152,33 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
     __syncthreads();
     for (uint64_t i = 0; i < ntl; i++) {
         const int slot = (int)(i % TP_NSLOT);
-        const uint64_t t0 = beg + i * TILE;
-        const int tn = (int)umin64((uint64_t)TILE, end - t0);
+        const uint64_t t0 = tbase + i * TILE;                       // (even)
+        const int th = (int)umin64((uint64_t)TILE, end - t0);       // slot positions [0, th) staged
+        const int lo = i == 0 ? (int)(beg - tbase) : 0;             // ... of which [lo, th) are ours
+        const int tn = th - lo;                                     // keys in this tile
         mbar_wait(&S.mbar[slot], (phase >> slot) & 1u);
         mark(0);
-        const uint64_t *keys = S.ring[slot] + (t0 & 1);
-        const uint16_t *bids = BIDS ? (*sb)[slot] + (t0 & 7) : nullptr;
+        const uint64_t *keys = S.ring[slot];                        // key t0 + h at keys[h]
+        const uint16_t *bids = BIDS ? (*sb)[slot] + (t0 & 7) : nullptr;  // (t0 & 7 even: 4-byte pairs)
         uint64_t key[KPT];
         uint32_t code[KPT];
 #pragma unroll
-        for (int k = 0; k < KPT; k++) {
-            const int idx = k * NT + tid;
-            code[k] = 0xffffffffu;
-            if (idx < tn) {
-                key[k] = keys[idx];
-                const uint32_t b = BIDS ? (uint32_t)bids[idx] : bf(key[k], t0 + idx);
-                if (!SKIP || b != TP_SKIP) {
-                    const uint32_t r = atomicAdd(&S.cnt[b], 1u);
-                    code[k] = b | (r << 10);
+        for (int k2 = 0; k2 < KPT / 2; k2++) {
+            const int h = 2 * (k2 * NT + tid);  // slot positions h, h + 1
+            const ulonglong2 kv = *reinterpret_cast<const ulonglong2 *>(keys + h);
+            const uint32_t ip = BIDS ? *reinterpret_cast<const uint32_t *>(bids + h) : 0u;
+            key[2 * k2] = kv.x;
+            key[2 * k2 + 1] = kv.y;
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const int k = 2 * k2 + e;
+                code[k] = 0xffffffffu;
+                if (h + e >= lo && h + e < th) {
+                    const uint32_t b = BIDS ? (e ? ip >> 16 : ip & 0xffffu) : bf(key[k], t0 + h + e);
+                    if (!SKIP || b != TP_SKIP) {
+                        const uint32_t r = atomicAdd(&S.cnt[b], 1u);
+                        code[k] = b | (r << 10);
+                    }
                 }
             }
         }
@@ -172,7 +187,7 @@ __device__ __forceinline__ void tile_partition(TpSmemT<NT, KPT> &S, const uint64
         // every thread is past the previous tile's store phase: its ring slot
         // is free for the tile after the next one
         if (tid == 0 && i >= 1 && i - 1 + TP_NSLOT < ntl) {
-            const uint64_t tp0 = beg + (i - 1 + TP_NSLOT) * TILE;
+            const uint64_t tp0 = tbase + (i - 1 + TP_NSLOT) * TILE;
             tp_issue<TpSmemT<NT, KPT>, SB>(S, (int)((i - 1) % TP_NSLOT), src, tp0, umin64(end, tp0 + TILE), len,
                      BIDS ? bid : nullptr, sb);
         }
@@ -301,8 +316,10 @@ __device__ __forceinline__ void tp_issue_first(SM &S, const uint64_t *src, uint6
     constexpr int TILE = SM::TILE;
     for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.mbar[j], 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (inits before the bulk copies)
-    for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && beg + j * TILE < end; j++)
-        tp_issue<SM, SB>(S, (int)j, src, beg + j * TILE, umin64(end, beg + (j + 1) * TILE), len, bid, sb);
+    if (end <= beg) return;
+    const uint64_t base = beg & ~1ull;  // (tile_partition's tiling: even tile starts)
+    for (uint64_t j = 0; j < (uint64_t)TP_NSLOT && base + j * TILE < end; j++)
+        tp_issue<SM, SB>(S, (int)j, src, base + j * TILE, umin64(end, base + (j + 1) * TILE), len, bid, sb);
 }
 
 template <class SM>
