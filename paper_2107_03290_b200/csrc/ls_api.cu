@@ -312,6 +312,27 @@ struct Timer {
     }
 };
 
+// A second stream per device (non-blocking), for work that runs beside the
+// main sequence inside one sort (forked and joined with events; captured into
+// the CUDA Graph as parallel branches). nullptr if it cannot be created.
+static cudaStream_t side_stream() {
+    constexpr int MAXD = 64;
+    static cudaStream_t s[MAXD];
+    static std::once_flag once[MAXD];
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXD) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::call_once(once[d], [d] {
+        if (cudaStreamCreateWithFlags(&s[d], cudaStreamNonBlocking) != cudaSuccess) {
+            s[d] = nullptr;
+            cudaGetLastError();
+        }
+    });
+    return s[d];
+}
+
 // The launch sequence of one sort, from the workspace initialisation to the
 // big path. Every data-dependent decision is taken on the device (task lists,
 // counters in Ctl), so the sequence depends only on its arguments.
@@ -367,9 +388,29 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     tm.mark(LS_PHASE_SCATTER1);
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
-    launch_bucketsort(a, dt, st);
-    launches += 6;
-    tm.mark(LS_PHASE_BUCKETSORT);
+    // in-bucket sort: k_warpsort on `st`, the CTA sorts and block windows
+    // beside it on the device's side stream (disjoint sub-buckets; the few
+    // CTA-sized tasks of smooth inputs are latency-bound, so serialised after
+    // the warp sort they cost ~60 us); joined before the big path
+    {
+        cudaStream_t s2 = side_stream();
+        cudaEvent_t ef = nullptr, ej = nullptr;
+        bool fork = s2 && cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) == cudaSuccess;
+        if (fork) LS_CUDA(cudaEventRecord(ef, st));
+        if (fork && cudaStreamWaitEvent(s2, ef, 0) != cudaSuccess) fork = false;  // (then all on st)
+        if (!fork) cudaGetLastError();
+        launch_warpsort(a, dt, st);
+        launch_bucketsort(a, dt, fork ? s2 : st);
+        launches += 6;
+        tm.mark(LS_PHASE_BUCKETSORT);  // (the warp sort; the rest is in the next phase if not hidden)
+        if (fork) {
+            LS_CUDA(cudaEventRecord(ej, s2));
+            LS_CUDA(cudaStreamWaitEvent(st, ej, 0));
+        }
+        if (ef) cudaEventDestroy(ef);
+        if (ej) cudaEventDestroy(ej);
+    }
     launch_big_minmax(a, dt, st);
     launches++;
     launch_large(a, dt, st);

@@ -331,6 +331,7 @@ struct Ctl {
     uint32_t nchunks;                  // k_big_minmax work entries
     uint32_t nwin, wticket;            // bucket-sort windows (k_window_list) / work counter
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
+    uint32_t sticket;                  // k_warpsort's task tickets (batches of WS_BATCH)
     uint32_t nctask, nctask2, nctask3; // CTA sub-bucket sorts: SC_CTA, SC_CTAM, SC_CTAL (k_classify)
     uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
     uint32_t nfill;                    // homogeneous pieces of large items (k_large_fill)

@@ -33,7 +33,8 @@ uint32_t round1_capacity();  // keys per cluster (0: clusters unavailable)
 void launch_round1(const Args &a, int dtype, cudaStream_t st);
 
 // in-bucket sort (ls_sortsub.cu)
-void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);
+void launch_warpsort(const Args &a, int dtype, cudaStream_t st);
+void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);  // the CTA sorts and block windows
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);
 void launch_big_order(const Args &a, cudaStream_t st);
 void launch_big(const Args &a, int dtype, cudaStream_t st);  // all levels, one cooperative launch

@@ -29,6 +29,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = 0;
+        ctl->sticket = 0;
         ctl->nfused = ctl->fticket = 0;
         ctl->exact0 = 0;
         ctl->nlarge = ctl->npiece = 0;

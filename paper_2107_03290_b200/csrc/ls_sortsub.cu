@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
 }
 
 // ------------------------------------------------------ warp sub-bucket sort --
+constexpr uint32_t WS_BATCH = 8;  // warp tasks per ticket
 template <int DT>
 __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args a) {
     if (a.ctl->status) return;
@@ -562,15 +563,27 @@ __global__ void __launch_bounds__(WS_WARPS * 32, WS_CTAS_PER_SM) k_warpsort(Args
     const Root R = load_root(a.M);
     const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
-    const uint32_t nw = gridDim.x * WS_WARPS;
     uint32_t r_maxg = 0;
     bool early_h1 = false;
-    uint4 nxt = blockIdx.x * WS_WARPS + warp < ntask ? a.tasks[blockIdx.x * WS_WARPS + warp]
-                                                       : make_uint4(0, 0, 0, 0);
-    for (uint32_t t = blockIdx.x * WS_WARPS + warp; t < ntask; t += nw) {
-        const uint4 task = nxt;
-        if (t + nw < ntask) nxt = a.tasks[t + nw];
-        ws_task<DT>(a, R, g_lo, g_hi, W, wst[warp], r_maxg, early_h1, task, lane);
+    // tasks taken in batches of WS_BATCH consecutive ones from a ticket
+    // counter (the next batch's ticket in flight during the current one):
+    // a warp that started late, or met slower sub-buckets, takes fewer, so
+    // every warp finishes within about one batch of the others (the other
+    // sorts of the phase run beside this kernel on a second stream)
+    uint32_t t0 = 0;
+    if (lane == 0) t0 = atomicAdd(&a.ctl->sticket, WS_BATCH);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    while (t0 < ntask) {
+        uint32_t tn = 0;
+        if (lane == 0) tn = atomicAdd(&a.ctl->sticket, WS_BATCH);
+        const uint32_t t1 = min(t0 + WS_BATCH, ntask);
+        uint4 nxt = a.tasks[t0];
+        for (uint32_t t = t0; t < t1; t++) {
+            const uint4 task = nxt;
+            if (t + 1 < t1) nxt = a.tasks[t + 1];
+            ws_task<DT>(a, R, g_lo, g_hi, W, wst[warp], r_maxg, early_h1, task, lane);
+        }
+        t0 = __shfl_sync(0xffffffffu, tn, 0);
     }
     if (lane == 0) {
         for (int q = 0; q < 4; q++)
@@ -1634,14 +1647,22 @@ static void launch_ctasort(const Args &a, int dtype, cudaStream_t st, const uint
     }
 }
 
+void launch_warpsort(const Args &a, int dtype, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = sms * WS_CTAS_PER_SM;
+    if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
+    else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
+}
+
+// The other sorts of the in-bucket phase (CTA sorts, block windows): every
+// one reads only its own sub-buckets, so they run beside k_warpsort.
 void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int g = sms * WS_CTAS_PER_SM;
-        if (dtype == DT_F64) k_warpsort<DT_F64><<<g, WS_WARPS * 32, 0, st>>>(a);
-        else k_warpsort<DT_U64><<<g, WS_WARPS * 32, 0, st>>>(a);
         launch_ctasort<256, 16, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
         launch_ctasort<128, 16, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
         launch_ctasort<128, 8, 8>(a, dtype, st, a.ctasks3, &a.ctl->nctask3, sms);
