@@ -356,13 +356,29 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
         launch_fit_params(l.m, l.L, a.ctl, a.leaf_cnt, a.leaf_min, a.M, dt, st);
         launches += 3;
     }
-    launch_b0_table(a.M, l.L, l.f, dt, st);
-    launches += 3;
     // round 0 by reservation: bucket capacities from the sample (k_cap0),
     // then one scatter pass; the exact count pass (k_count0 + plan +
-    // k_scatter0) runs only when a capacity did not hold (kernels exit early)
-    launch_cap0(a, l.m, dt, st);
-    launches += 2;
+    // k_scatter0) runs only when a capacity did not hold (kernels exit early).
+    // The capacities need only the model: they are computed on the side
+    // stream while the b0 search tables are built
+    {
+        cudaStream_t s2 = side_stream();
+        cudaEvent_t ef = nullptr, ej = nullptr;
+        bool fork = s2 && cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) == cudaSuccess;
+        if (fork) LS_CUDA(cudaEventRecord(ef, st));
+        if (fork && cudaStreamWaitEvent(s2, ef, 0) != cudaSuccess) fork = false;  // (then all on st)
+        if (!fork) cudaGetLastError();
+        launch_cap0(a, l.m, dt, fork ? s2 : st);
+        launch_b0_table(a.M, l.L, l.f, dt, st);
+        launches += 5;
+        if (fork) {
+            LS_CUDA(cudaEventRecord(ej, s2));
+            LS_CUDA(cudaStreamWaitEvent(st, ej, 0));
+        }
+        if (ef) cudaEventDestroy(ef);
+        if (ej) cudaEventDestroy(ej);
+    }
     tm.mark(LS_PHASE_FIT);
     launch_scatter0r(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, 1, st);

@@ -264,12 +264,12 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_scatter0(Args a) {
 // 5 standard deviations), the scatter reserves every tile's run in its bucket
 // with one atomicAdd, and the count pass (k_count0) runs only if a bucket
 // overflowed or the capacities did not fit B. S_B = the final cursors (exact).
-// The sample's level-0 histogram: b0 search tables staged in shared memory,
-// 8 independent keys per thread (the lookups of one key are a dependent
-// chain; a global-memory version with one key at a time was latency-bound:
-// 45 us for 2M keys at 200M).
+// The sample's level-0 histogram, b0 = bucket0(predict(x)) (O7) with the
+// leaf lines staged in shared memory: it needs only the fitted model, not the
+// b0 search tables, so it runs on the side stream while k_b0_* build them.
+// 8 independent keys per thread.
 struct SampHistSmem {
-    B0Smem b0;
+    double leaf[5 * LS_MAX_LEAVES];
     uint32_t h[LS_MAX_FANOUT];
 };
 constexpr int SH_THREADS = 512;
@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(SH_THREADS, 2) k_samp_hist0(Args a, uint64_t m
     SampHistSmem &S = *reinterpret_cast<SampHistSmem *>(smem_raw);
     const int f = a.f, tid = threadIdx.x;
     for (int b = tid; b < f; b += SH_THREADS) S.h[b] = 0;
-    const B0Search bs = load_b0_search(S.b0, a.M);
+    const int L = (int)a.M->L;
+    for (int i = tid; i < 5 * L; i += SH_THREADS) S.leaf[i] = a.M->leaf[i];
+    const Root R = load_root(a.M);
+    const double F = a.F;
     __syncthreads();
     constexpr int U = 8;
     const uint64_t gs = (uint64_t)gridDim.x * SH_THREADS * U;
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(SH_THREADS, 2) k_samp_hist0(Args a, uint64_t m
         for (int q = 0; q < U; q++) k[q] = i + q * SH_THREADS < m ? a.S[i + q * SH_THREADS] : 0ull;
 #pragma unroll
         for (int q = 0; q < U; q++)
-            if (i + q * SH_THREADS < m) atomicAdd(&S.h[bs.get<DT>(k[q])], 1u);
+            if (i + q * SH_THREADS < m) atomicAdd(&S.h[bucket0(predict<DT>(k[q], R, S.leaf), F, f)], 1u);
     }
     __syncthreads();
     for (int b = tid; b < f; b += SH_THREADS)
