@@ -44,7 +44,7 @@ struct Layout {
     size_t ctl, model, leaf_cnt, leaf_min, S, hist0, start0, bmin0, bmax0, ustart, lb0, offs0,
         hist1, start1, cur1, tfirst, tlast, wlist, tasks, big, chunks, hist1_u64, B, large, ltot,
         cap0, bsrc, cur0, shist0,
-        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, fused, flist,
+        lstart, lcur, lhom, lmin, lmax, pieces, bid, fills, ctasks, ctasks2, ctasks3, ctasks4, fused, flist,
         border;
     uint32_t task_cap, lcap, pcap, fcap;
     uint32_t chunk_cap;
@@ -121,6 +121,7 @@ static Layout make_layout(uint64_t n, const ls_config &cfg) {
     l.ctasks = take((size_t)l.task_cap * 16);
     l.ctasks2 = take((size_t)l.task_cap * 16);
     l.ctasks3 = take((size_t)l.task_cap * 16);
+    l.ctasks4 = take((size_t)l.task_cap * 16);
     l.fused = take((size_t)l.f * 4);
     l.flist = take((size_t)l.f * 4);
     l.large = take((size_t)l.lcap * 4);
@@ -195,6 +196,7 @@ static Args make_args(const Layout &l, void *d_keys, void *d_ws) {
     a.ctasks = (uint4 *)(w + l.ctasks);
     a.ctasks2 = (uint4 *)(w + l.ctasks2);
     a.ctasks3 = (uint4 *)(w + l.ctasks3);
+    a.ctasks4 = (uint4 *)(w + l.ctasks4);
     a.fused = (uint32_t *)(w + l.fused);
     a.flist = (uint32_t *)(w + l.flist);
     a.large = (uint32_t *)(w + l.large);
@@ -416,9 +418,12 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
         if (fork) LS_CUDA(cudaEventRecord(ef, st));
         if (fork && cudaStreamWaitEvent(s2, ef, 0) != cudaSuccess) fork = false;  // (then all on st)
         if (!fork) cudaGetLastError();
-        launch_warpsort(a, dt, st);
+        // (the side stream's kernels are enqueued first: their few working CTAs
+        // take SM slots before the persistent warp sort fills them, whose
+        // batched task tickets let late-starting warps simply take fewer)
         launch_bucketsort(a, dt, fork ? s2 : st);
-        launches += 6;
+        launch_warpsort(a, dt, st);
+        launches += 7;
         tm.mark(LS_PHASE_BUCKETSORT);  // (the warp sort; the rest is in the next phase if not hidden)
         if (fork) {
             LS_CUDA(cudaEventRecord(ej, s2));
@@ -747,8 +752,8 @@ ls_status finish_sort(Pending *pend, cudaStream_t st, ls_stats *stats) {
     if (getenv("LS_DEBUG_STAGE")) {
         fprintf(stderr, "prof:");
         for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", c.prof[i]);
-        fprintf(stderr, "\ntasks: warp %u cta4096 %u cta2048 %u cta1024 %u windows %u large %u\n",
-                c.ntask, c.nctask, c.nctask2, c.nctask3, c.nwin, c.nlarge);
+        fprintf(stderr, "\ntasks: warp %u cta4096 %u cta2048 %u cta1024 %u cta512 %u windows %u large %u\n",
+                c.ntask, c.nctask, c.nctask2, c.nctask3, c.nctask4, c.nwin, c.nlarge);
         fprintf(stderr, "big items per level: %u %u %u %u (first pass %u)\n", c.big_cnt[0], c.big_cnt[1],
                 c.big_cnt[2], c.big_cnt[3], c.big_lv0);
         if (pend->model_dev) {

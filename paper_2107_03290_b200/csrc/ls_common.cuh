@@ -300,7 +300,8 @@ constexpr int BIG_LEVELS = 6;
 constexpr uint32_t WS_MAX = 256;  // SMALL sub-buckets of WS_MIN+1..WS_MAX keys: one warp each (k_warpsort)
 constexpr uint32_t WS_MIN = 32;   // tiny sub-buckets (<= WS_MIN keys) go to the block windows, many per window
 constexpr uint32_t BW_MAX = 1024;  // sub-buckets up to this size fit the block windows (k_bucketsort)
-constexpr uint32_t CL_MAX = 1024;  // SMALL sub-buckets of WS_MAX+1..CL_MAX keys: 128-thread CTAs, 8 keys/thread
+constexpr uint32_t CS_S_MAX = 512;  // SMALL sub-buckets of WS_MAX+1..CS_S_MAX keys: 64-thread CTAs, 8 keys/thread
+constexpr uint32_t CL_MAX = 1024;  // SMALL sub-buckets of CS_S_MAX+1..CL_MAX keys: 128-thread CTAs, 8 keys/thread
 constexpr uint32_t CM_MAX = 2048;  // SMALL sub-buckets of CL_MAX+1..CM_MAX keys: 128-thread CTAs, 16 keys/thread
 constexpr uint32_t CS_MAX = 4096;  // SMALL sub-buckets of WS_MAX+1..CS_MAX keys: one CTA each (k_ctasort)
 // Size class of a sub-bucket of np keys (T_small = cfg.big_threshold):
@@ -308,12 +309,13 @@ constexpr uint32_t CS_MAX = 4096;  // SMALL sub-buckets of WS_MAX+1..CS_MAX keys
 //   257..1024 one 128-thread CTA (8 keys per thread); 1025..2048 one
 //   128-thread CTA (16 per thread); 2049..T_small one 256-thread CTA;
 //   > T_small the exact big path.
-enum { SC_TRIVIAL = 0, SC_WINDOW, SC_WARP, SC_CTAL, SC_CTAM, SC_CTA, SC_BIG, SC_FUSED };  // (SC_FUSED: sorted by k_round1)
+enum { SC_TRIVIAL = 0, SC_WINDOW, SC_WARP, SC_CTAS, SC_CTAL, SC_CTAM, SC_CTA, SC_BIG, SC_FUSED };  // (SC_FUSED: sorted by k_round1)
 __host__ __device__ __forceinline__ int size_class(uint32_t np, uint32_t T_small) {
     if (np <= 1) return SC_TRIVIAL;
     if (np > T_small) return SC_BIG;
     if (np <= WS_MIN) return SC_WINDOW;
     if (np <= WS_MAX) return SC_WARP;
+    if (np <= CS_S_MAX) return SC_CTAS;
     if (np <= CL_MAX) return SC_CTAL;
     if (np <= CM_MAX) return SC_CTAM;
     return SC_CTA;
@@ -333,6 +335,7 @@ struct Ctl {
     uint32_t ntask;                    // warp sub-bucket sorts (k_classify)
     uint32_t sticket;                  // k_warpsort's task tickets (batches of WS_BATCH)
     uint32_t nctask, nctask2, nctask3; // CTA sub-bucket sorts: SC_CTA, SC_CTAM, SC_CTAL (k_classify)
+    uint32_t nctask4;                  // ... SC_CTAS
     uint32_t nlarge, npiece;           // large big items (ls_bigpath.cu) / their small pieces
     uint32_t nfill;                    // homogeneous pieces of large items (k_large_fill)
     uint32_t nfused, fticket;          // cluster-resident round 1: buckets listed / taken
@@ -397,7 +400,7 @@ struct Args {
     uint4 *wlist;                     // [ntiles] non-empty windows {g0, g1, lo, hi}
     uint16_t *bid;                    // [n + 16] bucket id of each key, count -> scatter pass
     uint4 *tasks;                     // [task_cap] warp sub-bucket sorts {start, n', g, 0}
-    uint4 *ctasks, *ctasks2, *ctasks3;// [task_cap] CTA sub-bucket sorts {start, n', g, 0}
+    uint4 *ctasks, *ctasks2, *ctasks3, *ctasks4;// [task_cap] CTA sub-bucket sorts {start, n', g, 0}
     uint32_t task_cap;
     // large big items (> LARGE_MIN keys): per item 1024-digit tables
     uint32_t *large;                  // [lcap] index into big[] (level 0)

@@ -28,7 +28,7 @@ __global__ void k_init(Ctl *ctl) {
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
-        ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = 0;
+        ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = ctl->nctask4 = 0;
         ctl->sticket = 0;
         ctl->nfused = ctl->fticket = 0;
         ctl->exact0 = 0;
@@ -621,17 +621,18 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
     // warp / CTA sorts become task lists (compacted per block: one global
     // atomic per level-0 bucket and class)
     {
-        __shared__ uint32_t wcnt[4][32], wbase[4];
+        __shared__ uint32_t wcnt[5][32], wbase[5];
         const int lane = tid & 31, w = tid >> 5;
-        uint32_t m[4];
+        uint32_t m[5];
         m[0] = __ballot_sync(0xffffffffu, sc == SC_WARP);
         m[1] = __ballot_sync(0xffffffffu, sc == SC_CTA);
         m[2] = __ballot_sync(0xffffffffu, sc == SC_CTAM);
         m[3] = __ballot_sync(0xffffffffu, sc == SC_CTAL);
+        m[4] = __ballot_sync(0xffffffffu, sc == SC_CTAS);
         if (lane == 0)
-            for (int q = 0; q < 4; q++) wcnt[q][w] = __popc(m[q]);
+            for (int q = 0; q < 5; q++) wcnt[q][w] = __popc(m[q]);
         __syncthreads();
-        if (tid < 4) {
+        if (tid < 5) {
             uint32_t tot = 0;
             for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
                 const uint32_t t = wcnt[tid][q];
@@ -639,17 +640,17 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
                 tot += t;
             }
             uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask
-                          : tid == 2 ? &a.ctl->nctask2 : &a.ctl->nctask3;
+                          : tid == 2 ? &a.ctl->nctask2 : tid == 3 ? &a.ctl->nctask3 : &a.ctl->nctask4;
             wbase[tid] = tot ? atomicAdd(ctr, tot) : 0u;
         }
         __syncthreads();
-        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : sc == SC_CTAL ? 3 : -1;
+        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : sc == SC_CTAL ? 3 : sc == SC_CTAS ? 4 : -1;
         // warp tasks carry the leaf that holds all their keys (+1; 0: none)
         const uint32_t wl = m[0] ? contained_leaf_warp(a.M->leaf, (int)a.M->L, (uint32_t)(row + (tid & ~31)),
                                                        (uint32_t)g, a.rcpF2, lane) : 0u;
         if (c2 >= 0) {
             const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m[c2] & ((1u << lane) - 1u));
-            uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : c2 == 2 ? a.ctasks2 : a.ctasks3;
+            uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : c2 == 2 ? a.ctasks2 : c2 == 3 ? a.ctasks3 : a.ctasks4;
             if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, c2 == 0 ? wl : 0u);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }

@@ -1666,6 +1666,7 @@ void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
         launch_ctasort<256, 16, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
         launch_ctasort<128, 16, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
         launch_ctasort<128, 8, 8>(a, dtype, st, a.ctasks3, &a.ctl->nctask3, sms);
+        launch_ctasort<64, 8, 16>(a, dtype, st, a.ctasks4, &a.ctl->nctask4, sms);
     }
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
