@@ -314,25 +314,27 @@ struct Timer {
     }
 };
 
-// A second stream per device (non-blocking), for work that runs beside the
+// Side streams per device (non-blocking), for work that runs beside the
 // main sequence inside one sort (forked and joined with events; captured into
-// the CUDA Graph as parallel branches). nullptr if it cannot be created.
-static cudaStream_t side_stream() {
+// the CUDA Graph as parallel branches). nullptr if one cannot be created.
+constexpr int LS_NSIDE = 5;
+static cudaStream_t side_stream(int k = 0) {
     constexpr int MAXD = 64;
-    static cudaStream_t s[MAXD];
+    static cudaStream_t s[MAXD][LS_NSIDE];
     static std::once_flag once[MAXD];
     int d = -1;
-    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXD) {
+    if (k < 0 || k >= LS_NSIDE || cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXD) {
         cudaGetLastError();
         return nullptr;
     }
     std::call_once(once[d], [d] {
-        if (cudaStreamCreateWithFlags(&s[d], cudaStreamNonBlocking) != cudaSuccess) {
-            s[d] = nullptr;
-            cudaGetLastError();
-        }
+        for (int j = 0; j < LS_NSIDE; j++)
+            if (cudaStreamCreateWithFlags(&s[d][j], cudaStreamNonBlocking) != cudaSuccess) {
+                s[d][j] = nullptr;
+                cudaGetLastError();
+            }
     });
-    return s[d];
+    return s[d][k];
 }
 
 // The launch sequence of one sort, from the workspace initialisation to the
@@ -411,26 +413,39 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     // CTA-sized tasks of smooth inputs are latency-bound, so serialised after
     // the warp sort they cost ~60 us); joined before the big path
     {
-        cudaStream_t s2 = side_stream();
-        cudaEvent_t ef = nullptr, ej = nullptr;
-        bool fork = s2 && cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) == cudaSuccess &&
-                    cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) == cudaSuccess;
+        // one side stream per CTA-sort shape (and one for the block windows):
+        // k_warpsort's 4 CTAs per SM fill the register file, so a side kernel
+        // queued behind another on one stream finds no SM until the warp sort
+        // retires; on separate streams they all take their slots first
+        cudaStream_t ss[LS_NSIDE];
+        cudaEvent_t ef = nullptr, ej[LS_NSIDE] = {};
+        bool fork = cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) == cudaSuccess;
+        for (int j = 0; j < LS_NSIDE; j++) {
+            ss[j] = side_stream(j);
+            fork = fork && ss[j] && cudaEventCreateWithFlags(&ej[j], cudaEventDisableTiming) == cudaSuccess;
+        }
         if (fork) LS_CUDA(cudaEventRecord(ef, st));
-        if (fork && cudaStreamWaitEvent(s2, ef, 0) != cudaSuccess) fork = false;  // (then all on st)
-        if (!fork) cudaGetLastError();
-        // (the side stream's kernels are enqueued first: their few working CTAs
-        // take SM slots before the persistent warp sort fills them, whose
+        for (int j = 0; fork && j < LS_NSIDE; j++)
+            if (cudaStreamWaitEvent(ss[j], ef, 0) != cudaSuccess) fork = false;  // (then all on st)
+        if (!fork) {
+            cudaGetLastError();
+            for (int j = 0; j < LS_NSIDE; j++) ss[j] = st;
+        }
+        // (the side streams' kernels are enqueued first: their few working
+        // CTAs take SM slots before the persistent warp sort fills them, whose
         // batched task tickets let late-starting warps simply take fewer)
-        launch_bucketsort(a, dt, fork ? s2 : st);
+        launch_bucketsort(a, dt, ss);
         launch_warpsort(a, dt, st);
         launches += 7;
         tm.mark(LS_PHASE_BUCKETSORT);  // (the warp sort; the rest is in the next phase if not hidden)
-        if (fork) {
-            LS_CUDA(cudaEventRecord(ej, s2));
-            LS_CUDA(cudaStreamWaitEvent(st, ej, 0));
-        }
+        if (fork)
+            for (int j = 0; j < LS_NSIDE; j++) {
+                LS_CUDA(cudaEventRecord(ej[j], ss[j]));
+                LS_CUDA(cudaStreamWaitEvent(st, ej[j], 0));
+            }
         if (ef) cudaEventDestroy(ef);
-        if (ej) cudaEventDestroy(ej);
+        for (int j = 0; j < LS_NSIDE; j++)
+            if (ej[j]) cudaEventDestroy(ej[j]);
     }
     launch_big_minmax(a, dt, st);
     launches++;

@@ -34,7 +34,7 @@ void launch_round1(const Args &a, int dtype, cudaStream_t st);
 
 // in-bucket sort (ls_sortsub.cu)
 void launch_warpsort(const Args &a, int dtype, cudaStream_t st);
-void launch_bucketsort(const Args &a, int dtype, cudaStream_t st);  // the CTA sorts and block windows
+void launch_bucketsort(const Args &a, int dtype, const cudaStream_t st[5]);  // the CTA sorts (st[0..3]) and block windows (st[4])
 void launch_big_minmax(const Args &a, int dtype, cudaStream_t st);
 void launch_big_order(const Args &a, cudaStream_t st);
 void launch_big(const Args &a, int dtype, cudaStream_t st);  // all levels, one cooperative launch

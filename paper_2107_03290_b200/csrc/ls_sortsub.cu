@@ -1658,16 +1658,17 @@ void launch_warpsort(const Args &a, int dtype, cudaStream_t st) {
 
 // The other sorts of the in-bucket phase (CTA sorts, block windows): every
 // one reads only its own sub-buckets, so they run beside k_warpsort.
-void launch_bucketsort(const Args &a, int dtype, cudaStream_t st) {
+void launch_bucketsort(const Args &a, int dtype, const cudaStream_t ss[5]) {
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        launch_ctasort<256, 16, 3>(a, dtype, st, a.ctasks, &a.ctl->nctask, sms);
-        launch_ctasort<128, 16, 6>(a, dtype, st, a.ctasks2, &a.ctl->nctask2, sms);
-        launch_ctasort<128, 8, 8>(a, dtype, st, a.ctasks3, &a.ctl->nctask3, sms);
-        launch_ctasort<64, 8, 16>(a, dtype, st, a.ctasks4, &a.ctl->nctask4, sms);
+        launch_ctasort<256, 16, 3>(a, dtype, ss[0], a.ctasks, &a.ctl->nctask, sms);
+        launch_ctasort<128, 16, 6>(a, dtype, ss[1], a.ctasks2, &a.ctl->nctask2, sms);
+        launch_ctasort<128, 8, 8>(a, dtype, ss[2], a.ctasks3, &a.ctl->nctask3, sms);
+        launch_ctasort<64, 8, 16>(a, dtype, ss[3], a.ctasks4, &a.ctl->nctask4, sms);
     }
+    const cudaStream_t st = ss[4];
     k_window_list<<<(a.ntiles + 255) / 256, 256, 0, st>>>(a);
     const size_t sm = sizeof(BsSmem);
     int dev = 0, sms = 148;
