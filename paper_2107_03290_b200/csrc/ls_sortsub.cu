@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(BS_THREADS, BS_CTAS_PER_SM) k_bucketsort(Args 
                 if (size_class(np, a.T_small) == SC_WINDOW && (uint32_t)i - h < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
                     const double adj = adj_of(e & 0xfffffu, a.F2, rcpF2);  // (i*f + j)/f^2
-                    sl = h + cs_pos(p, adj, a.nd, (int)(np - 1u));
+                    // (the p-range spread over the n' slots, as in k_ctasort)
+                    sl = h + cs_pos(p, adj, __dmul_rn(a.F2, (double)np), (int)(np - 1u));
                 }
                 // warp-aggregated: keys of equal slot (duplicates!) take one atomic
                 const uint32_t peers = __match_any_sync(__activemask(), sl);
@@ -672,6 +673,13 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
         const int top = (int)(np - 1u);
+        // slots: the sub-bucket's p-range [adj, adj + 1/f^2) spread over its
+        // n' slots, pos = floor((p - adj) * f^2 n') clamped to [0, n'-1]
+        // (Alg. 2's pos spreads it over n/f^2 slots: a sub-bucket
+        // larger than n/f^2 then fills only its first n/f^2 slots, and a
+        // smaller one piles every key past slot n'-1 into the last slot, R5).
+        // Monotone in p, so the counting sort + touch-up give R5's result.
+        const double nsl = __dmul_rn(a.F2, (double)np);
         uint32_t code[CS_KPT];
         if (g != g_lo && g != g_hi) {  // keys inside [xmin, xmax]: no root clamp
 #pragma unroll
@@ -679,7 +687,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 code[k] = BS_NONE;
                 if ((uint32_t)(k * CS_THREADS + tid) < np) {
                     const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
-                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t pos = cs_pos(p, adj, nsl, top);
                     const uint32_t r = atomicAdd(&S.K[pos], 1u);
                     code[k] = pos | (r << 12);
                 }
@@ -690,7 +698,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 code[k] = BS_NONE;
                 if ((uint32_t)(k * CS_THREADS + tid) < np) {
                     const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
-                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t pos = cs_pos(p, adj, nsl, top);
                     const uint32_t r = atomicAdd(&S.K[pos], 1u);
                     code[k] = pos | (r << 12);
                 }

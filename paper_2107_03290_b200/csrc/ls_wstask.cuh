@@ -103,15 +103,17 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
             return;
         }
     }
-    // Slots of the counting sort: pos = floor((p - adj) * n) (Alg. 2
-    // P:188-190) clamped to [0, S-1] with S = max(n', ceil(n/f^2) + 1)
-    // <= WS_MAX: R5 clamps to n'-1, which piles every key with pos >= n'-1
-    // of a sub-bucket smaller than n/f^2 into the last slot (one sorting
-    // network per such sub-bucket). The wider clamp refines R5's order (R5's
-    // pos = min(pos, n'-1), a monotone function of this one), so the
-    // placement is R5's counting sort with that top group already ordered
-    // by its unclamped positions; the touch-up finishes both identically.
-    const uint32_t S = max(np, min(a.S1, WS_MAX));
+    // Slots of the counting sort: Alg. 2's pos = floor((p - adj) * n)
+    // spreads the sub-bucket's p-range [adj, adj + 1/f^2) over
+    // ~n/f^2 slots and R5 clamps it to n'-1. Here the range is spread over
+    // all WS_MAX = 256 counters of the warp instead: pos = floor((p - adj) *
+    // 256 f^2) clamped to [0, 255]. Any pos that is monotone in p orders the
+    // keys of different slots (R15), and the touch-up sorts each slot's
+    // group, so the result is R5's: n/f^2 ~ 200 at 200M keys gets 1.28x finer
+    // slots (smaller collision groups, fewer odd-even passes), and n/f^2 >
+    // 256 (10^9 keys: ~1000) no longer piles every key with pos >= 255 into
+    // the last slot, where it met the warp bitonic.
+    const uint32_t S = WS_MAX;
     *reinterpret_cast<uint4 *>(&W.K[8 * lane]) = make_uint4(0, 0, 0, 0);  // K[0..256)
     *reinterpret_cast<uint4 *>(&W.K[8 * lane + 4]) = make_uint4(0, 0, 0, 0);
     __syncwarp();
@@ -120,6 +122,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
     // [xmin, xmax]; elsewhere the root clamp is skipped.
     const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
     const int top = (int)(S - 1u);
+    const double nsl = __dmul_rn(a.F2, (double)WS_MAX);  // slots per unit of p
     uint32_t code[WS_KPL];
     if (task.w != 0u && g != g_lo && g != g_hi) {
         // one leaf holds every key and p = its line value (k_classify's
@@ -131,7 +134,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
             code[k] = BS_NONE;
             if (32u * k + lane < np) {
                 const double p = __fma_rn(la, __dsub_rn(xd<DT>(key[k]), lc), lb);
-                const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                const uint32_t pos = cs_pos(p, adj, nsl, top);
                 const uint32_t r = atomicAdd(&W.K[pos], 1u);
                 code[k] = pos | (r << 16);
             }
@@ -162,7 +165,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
                 if (32u * k + lane < np) {
                     const double y = __fma_rn(la, __dsub_rn(xd<DT>(key[k]), lc), lb);
                     const double p = __dadd_rn(clampd(y, llo, lhi), 0.0);
-                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t pos = cs_pos(p, adj, nsl, top);
                     const uint32_t r = atomicAdd(&W.K[pos], 1u);
                     code[k] = pos | (r << 16);
                 }
@@ -173,7 +176,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
                 code[k] = BS_NONE;
                 if (32u * k + lane < np) {
                     const double p = predict_ldg_inner<DT>(key[k], R, a.M->leaf);
-                    const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                    const uint32_t pos = cs_pos(p, adj, nsl, top);
                     const uint32_t r = atomicAdd(&W.K[pos], 1u);
                     code[k] = pos | (r << 16);
                 }
@@ -185,7 +188,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
             code[k] = BS_NONE;
             if (32u * k + lane < np) {
                 const double p = predict_ldg<DT>(key[k], R, a.M->leaf);
-                const uint32_t pos = cs_pos(p, adj, a.nd, top);
+                const uint32_t pos = cs_pos(p, adj, nsl, top);
                 const uint32_t r = atomicAdd(&W.K[pos], 1u);
                 code[k] = pos | (r << 16);
             }
@@ -193,7 +196,7 @@ __device__ __forceinline__ void ws_task(const Args &a, const Root &R, uint32_t g
     }
     __syncwarp();
     // exclusive running totals over the S <= 256 slots, 8 per lane (two
-    // 16-byte loads / stores); K[S] = n' (for S < 256 the scan writes it)
+    // 16-byte loads / stores); K[256] = n'
     uint32_t mgs;  // largest collision group of <= BS_RANKMAX keys
     {
         const uint4 c0 = *reinterpret_cast<const uint4 *>(&W.K[8 * lane]);
