@@ -646,12 +646,14 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
         __syncthreads();
         const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : sc == SC_CTAL ? 3 : sc == SC_CTAS ? 4 : -1;
         // warp tasks carry the leaf that holds all their keys (+1; 0: none)
-        const uint32_t wl = m[0] ? contained_leaf_warp(a.M->leaf, (int)a.M->L, (uint32_t)(row + (tid & ~31)),
-                                                       (uint32_t)g, a.rcpF2, lane) : 0u;
+        const uint32_t wl = (m[0] | m[1] | m[2] | m[3] | m[4])
+                                ? contained_leaf_warp(a.M->leaf, (int)a.M->L, (uint32_t)(row + (tid & ~31)),
+                                                      (uint32_t)g, a.rcpF2, lane)
+                                : 0u;
         if (c2 >= 0) {
             const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m[c2] & ((1u << lane) - 1u));
             uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : c2 == 2 ? a.ctasks2 : c2 == 3 ? a.ctasks3 : a.ctasks4;
-            if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, c2 == 0 ? wl : 0u);
+            if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, wl);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }
     }

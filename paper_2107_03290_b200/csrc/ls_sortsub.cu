@@ -612,7 +612,6 @@ template <int CAP>
 struct CsSmem {
     uint64_t T[CAP + CAP / 8];
     alignas(16) uint32_t K[CAP + 8];
-    uint16_t slot_of[CAP];
     uint32_t big[BS_MAXBIG];
     uint32_t wsum[33];
     uint32_t nbig, ovf, mgs;
@@ -667,21 +666,39 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 continue;
             }
         }
-        for (uint32_t i = 4 * tid; i <= np; i += 4 * CS_THREADS)  // (K has CAP + 8 entries)
-            *reinterpret_cast<uint4 *>(&S.K[i]) = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < CS_KPT / 4; i++)  // K[0..CAP): thread tid owns slots CS_KPT*tid..
+            *reinterpret_cast<uint4 *>(&S.K[CS_KPT * tid + 4 * i]) = make_uint4(0, 0, 0, 0);
         if (tid == 0) S.nbig = S.ovf = S.mgs = S.nhuge = 0;
         __syncthreads();
         const double adj = adj_of(g, a.F2, a.rcpF2);  // (i*f + j)/f^2
-        const int top = (int)(np - 1u);
-        // slots: the sub-bucket's p-range [adj, adj + 1/f^2) spread over its
-        // n' slots, pos = floor((p - adj) * f^2 n') clamped to [0, n'-1]
-        // (Alg. 2's pos spreads it over n/f^2 slots: a sub-bucket
-        // larger than n/f^2 then fills only its first n/f^2 slots, and a
-        // smaller one piles every key past slot n'-1 into the last slot, R5).
-        // Monotone in p, so the counting sort + touch-up give R5's result.
-        const double nsl = __dmul_rn(a.F2, (double)np);
+        const int top = CAP - 1;
+        // slots: the sub-bucket's p-range [adj, adj + 1/f^2) spread over the
+        // CTA's CAP >= n' counters, pos = floor((p - adj) * f^2 CAP) clamped
+        // to [0, CAP-1] (Alg. 2's pos spreads it over n/f^2 slots, P:188-190:
+        // a sub-bucket larger than n/f^2 then fills only its first n/f^2
+        // slots, and a smaller one piles every key past slot n'-1 into the
+        // last slot, R5). Monotone in p, so the counting sort + touch-up give
+        // R5's result (reading R-SLOT); the scan below covers CAP slots as
+        // CS_KPT per thread, vector loads without bank conflicts.
+        const double nsl = __dmul_rn(a.F2, (double)CAP);
         uint32_t code[CS_KPT];
-        if (g != g_lo && g != g_hi) {  // keys inside [xmin, xmax]: no root clamp
+        if (task.w != 0u && g != g_lo && g != g_hi) {
+            // one leaf holds every key and p = its line value (k_classify's
+            // contained_leaf_warp, as in the warp sort: no routing, no clamp)
+            const double *q = a.M->leaf + 5 * (task.w - 1u);
+            const double la = __ldg(q), lc = __ldg(q + 1), lb = __ldg(q + 2);
+#pragma unroll
+            for (int k = 0; k < CS_KPT; k++) {
+                code[k] = BS_NONE;
+                if ((uint32_t)(k * CS_THREADS + tid) < np) {
+                    const double p = __fma_rn(la, __dsub_rn(xd<DT>(key[k]), lc), lb);
+                    const uint32_t pos = cs_pos(p, adj, nsl, top);
+                    const uint32_t r = atomicAdd(&S.K[pos], 1u);
+                    code[k] = pos | (r << 12);
+                }
+            }
+        } else if (g != g_lo && g != g_hi) {  // keys inside [xmin, xmax]: no root clamp
 #pragma unroll
             for (int k = 0; k < CS_KPT; k++) {
                 code[k] = BS_NONE;
@@ -705,21 +722,32 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
         }
         __syncthreads();
-        // exclusive running totals over np + 1 <= 4097 entries: each thread a
-        // contiguous segment of ceil((np + 1) / 256) entries (cost ~ np)
+        // exclusive running totals over the CAP slots, CS_KPT consecutive
+        // slots per thread (16-byte loads and stores); K[CAP] = n'
         {
-            const uint32_t per = (np + CS_THREADS) / CS_THREADS;
-            const uint32_t b0 = per * tid, b1 = min(b0 + per, np + 1u);
+            uint32_t c[CS_KPT];
+#pragma unroll
+            for (int i = 0; i < CS_KPT / 4; i++) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(&S.K[CS_KPT * tid + 4 * i]);
+                c[4 * i] = v.x;
+                c[4 * i + 1] = v.y;
+                c[4 * i + 2] = v.z;
+                c[4 * i + 3] = v.w;
+            }
             uint32_t sum = 0, mg = 0, mgs = 0;
-            for (uint32_t idx = b0; idx < b1; idx++) {
-                const uint32_t c = idx < np ? S.K[idx] : 0u;
-                mg = c > mg ? c : mg;
-                mgs = (c <= BS_RANKMAX && c > mgs) ? c : mgs;
-                if (c > BS_RANKMAX) {
-                    const uint32_t j = atomicAdd(&S.nbig, 1u);
-                    if (j < BS_MAXBIG) S.big[j] = idx; else S.ovf = 1;
-                }
-                sum += c;
+#pragma unroll
+            for (int q = 0; q < CS_KPT; q++) {
+                mg = max(mg, c[q]);
+                mgs = (c[q] <= BS_RANKMAX && c[q] > mgs) ? c[q] : mgs;
+                sum += c[q];
+            }
+            if (mg > BS_RANKMAX) {  // (duplicate-heavy inputs) list the groups > 8 keys
+#pragma unroll
+                for (int q = 0; q < CS_KPT; q++)
+                    if (c[q] > BS_RANKMAX) {
+                        const uint32_t j = atomicAdd(&S.nbig, 1u);
+                        if (j < BS_MAXBIG) S.big[j] = CS_KPT * tid + q; else S.ovf = 1;
+                    }
             }
             mg = __reduce_max_sync(0xffffffffu, mg);
             mgs = __reduce_max_sync(0xffffffffu, mgs);
@@ -734,11 +762,16 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
             }
             __syncthreads();
             uint32_t run = S.wsum[warp] + incl - sum;
-            for (uint32_t idx = b0; idx < b1; idx++) {
-                const uint32_t c = idx < np ? S.K[idx] : 0u;
-                S.K[idx] = run;
-                run += c;
+#pragma unroll
+            for (int i = 0; i < CS_KPT / 4; i++) {
+                uint4 v;
+                v.x = run; run += c[4 * i];
+                v.y = run; run += c[4 * i + 1];
+                v.z = run; run += c[4 * i + 2];
+                v.w = run; run += c[4 * i + 3];
+                *reinterpret_cast<uint4 *>(&S.K[CS_KPT * tid + 4 * i]) = v;
             }
+            if (tid == 0) S.K[CAP] = np;
         }
         __syncthreads();
         // placement
@@ -748,7 +781,6 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                 const uint32_t pos = code[k] & 0xfffu;
                 const uint32_t q = S.K[pos] + (code[k] >> 12);
                 T[q] = to_ord<DT>(key[k]);
-                S.slot_of[q] = (uint16_t)pos;
             }
         }
         __syncthreads();
@@ -792,9 +824,20 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
                     }
                 }
             }
-            // a small group straddling two warps' 256-position ranges
-            if (lane == 0 && row_i > 0 && q0 < np && S.slot_of[q0 - 1] == S.slot_of[q0]) {
-                const uint32_t sl = S.slot_of[q0], c = S.K[sl + 1] - S.K[sl];
+            // a small group straddling two warps' 256-position ranges: the
+            // group holding position q0 (the last slot sl with K[sl] <= q0,
+            // by bisection over the totals) starts before q0
+            uint32_t sl = 0;
+            if (lane == 0 && row_i > 0 && q0 < np) {
+                uint32_t lo = 0, n = CAP;  // K[0] = 0 <= q0; K[CAP] = n' > q0
+                while (n > 1) {
+                    const uint32_t h = n >> 1;
+                    if (S.K[lo + h] <= q0) { lo += h; n -= h; } else { n = h; }
+                }
+                sl = lo;
+            }
+            if (lane == 0 && row_i > 0 && q0 < np && S.K[sl] < q0) {
+                const uint32_t c = S.K[sl + 1] - S.K[sl];
                 if (c <= BS_RANKMAX) {
                     const uint32_t j = atomicAdd(&S.nbig, 1u);
                     if (j < BS_MAXBIG) S.big[j] = sl; else S.ovf = 1;
@@ -805,7 +848,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         // listed groups: one warp each
         {
             const uint32_t nb = min(S.nbig, (uint32_t)BS_MAXBIG);
-            const uint32_t extra = S.ovf ? np : 0u;
+            const uint32_t extra = S.ovf ? (uint32_t)CAP : 0u;
             for (uint32_t k = warp; k < nb + extra; k += CS_THREADS / 32) {
                 uint32_t sl;
                 if (k < nb) {
