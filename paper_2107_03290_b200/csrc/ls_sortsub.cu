@@ -636,6 +636,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
     const uint32_t g_lo = sub_bucket_at(R.xmin, R, a.M->leaf, a.F, a.F2, a.f);
     const uint32_t g_hi = sub_bucket_at(R.xmax, R, a.M->leaf, a.F, a.F2, a.f);
     if (tid < 5) S.st[tid] = 0;
+    bool early_h1 = false;  // (block-uniform)
     for (uint32_t t = blockIdx.x; t < ntask; t += gridDim.x) {
         const uint4 task = list[t];
         const uint32_t st = task.x, np = task.y, g = task.z;
@@ -648,8 +649,12 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         for (int k = 0; k < CS_KPT; k++) {
             key[k] = (uint32_t)(k * CS_THREADS + tid) < np ? gl[k * CS_THREADS] : 0ull;
         }
-        // homogeneous sub-bucket (all keys equal): nothing to sort or store
-        {
+        // homogeneous sub-bucket (all keys equal): nothing to sort or
+        // store. Tested up front only once this CTA has met one (as in the
+        // warp sort: the first == last test after the sort catches every
+        // case, and on inputs without such sub-buckets the up-front test is a
+        // block barrier per task for nothing)
+        if (early_h1) {
             const uint64_t k0 = a.A[st];
             bool diff = false;
 #pragma unroll
@@ -909,6 +914,7 @@ __global__ void __launch_bounds__(CS_THREADS, CS_CTAS_PER_SM) k_ctasort(Args a, 
         __syncthreads();
         // homogeneous iff first == last of the sorted sub-bucket
         const bool homog = T[0] == T[np - 1u];
+        early_h1 |= homog;
         if (!homog) {
             // T[k * CS_THREADS + tid] at tl[k * CS_THREADS * 9 / 8] (CS_THREADS % 8 == 0)
             const uint64_t *tl = S.T + tid + (tid >> 3);
