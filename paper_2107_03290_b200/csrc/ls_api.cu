@@ -1,5 +1,6 @@
 // ls_api.cu -- C ABI of libls (include/ls.h): workspace layout, the launch
 // sequence of Alg. 2 on one GPU, status/stats, and the parity hooks.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -280,6 +281,21 @@ static bool model_ok(const ls_model &m, const ls_config &cfg) {
     return true;
 }
 
+// NVTX ranges over the host-side enqueue of each phase (a profiler's timeline
+// shows which launches belong to which step of Alg. 1/2; a no-op without a
+// tool attached). Under graph capture they cover the capture, not the replay.
+struct NvtxPhase {
+    bool open = false;
+    void next(const char *name) {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    ~NvtxPhase() {
+        if (open) nvtxRangePop();
+    }
+};
+
 struct Timer {
     bool on = false;
     bool external = false;  // under stream capture: event-record nodes of the graph
@@ -346,6 +362,8 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     unsigned char *w = (unsigned char *)d_ws;
     LS_CUDA(cudaMemsetAsync(w + l.ff_begin, 0xff, l.ff_end - l.ff_begin, st));
     LS_CUDA(cudaMemsetAsync(w + l.zero_begin, 0, l.zero_end - l.zero_begin, st));
+    NvtxPhase nv;
+    nv.next("ls_sort: sample + fit");
     launch_init(a, st);
     launches++;
     if (inject) {
@@ -384,15 +402,18 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
         if (ej) cudaEventDestroy(ej);
     }
     tm.mark(LS_PHASE_FIT);
+    nv.next("ls_sort: round 0 (scatter0r)");
     launch_scatter0r(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, 1, st);
     launches += 2;
     tm.mark(LS_PHASE_SCATTER0);
+    nv.next("ls_sort: round 0 exact redo (count0 + scatter0)");
     launch_count0(a, dt, st);
     launch_plan0(a, dumps ? dumps->d_S_B : nullptr, 0, st);
     launch_scatter0(a, dt, st);
     launches += 3;
     tm.mark(LS_PHASE_COUNT0);
+    nv.next("ls_sort: round 1 count (count1)");
     if (a.fr_min) {  // buckets that fit a CTA cluster: count + scatter of round 1 in one kernel
         launch_round1(a, dt, st);
         launches++;
@@ -400,12 +421,15 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
     launch_count1(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_COUNT1);
+    nv.next("ls_sort: classify");
     launch_classify(a, nullptr, st);  // also turns count1's per-unit counts into offsets
     launches++;
     tm.mark(LS_PHASE_CLASSIFY);
+    nv.next("ls_sort: round 1 scatter (scatter1)");
     launch_scatter1(a, dt, st);
     launches++;
     tm.mark(LS_PHASE_SCATTER1);
+    nv.next("ls_sort: in-bucket sort");
     if (dumps && dumps->d_S_B1)
         LS_CUDA(cudaMemcpyAsync(dumps->d_S_B1, a.hist1, (size_t)l.f * l.f * 4, cudaMemcpyDeviceToDevice, st));
     // in-bucket sort: k_warpsort on `st`, the CTA sorts and block windows
@@ -437,7 +461,8 @@ static ls_status launch_sequence(Args &a, const Layout &l, const ls_config &cfg,
         launch_bucketsort(a, dt, ss);
         launch_warpsort(a, dt, st);
         launches += 7;
-        tm.mark(LS_PHASE_BUCKETSORT);  // (the warp sort; the rest is in the next phase if not hidden)
+        tm.mark(LS_PHASE_BUCKETSORT);
+        nv.next("ls_sort: big path");  // (the warp sort; the rest is in the next phase if not hidden)
         if (fork)
             for (int j = 0; j < LS_NSIDE; j++) {
                 LS_CUDA(cudaEventRecord(ej[j], ss[j]));

@@ -571,6 +571,15 @@ ls_status ls_sort_multi(ls_comm *comm, const void *d_in, uint64_t n_in, void *d_
     rc = enqueue_sort((uint64_t *)d_out, nout, dtype, &cfg, nullptr, w + l.local, ws_bytes - l.local, st, stats, nullptr, &pend);
     if (rc != LS_OK) return rc;
     rc = finish_sort(&pend, st, stats);
+    {   // a collective that failed after it was enqueued (a peer died, a link
+        // error) is reported by the communicator, not by the calls above
+        ncclResult_t ar = ncclSuccess;
+        NCCL_CHECK(ncclCommGetAsyncError(comm->comm, &ar));
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            set_error(ncclGetErrorString(ar));
+            return LS_E_NCCL;
+        }
+    }
     if (stats) {
         stats->peer_scatter = peer ? 1u : 0u;
         uint64_t rk = 0;
