@@ -582,10 +582,60 @@ __global__ void __launch_bounds__(NT, TP_THREADS / NT) k_scatter1(Args a) {
 // ------------------------------------------------------------- classify ----
 // Per level-0 bucket b (one block): H0, S'_B row, sub-bucket starts,
 // H1 for n' <= 1, SMALL -> bucket-sort tiles, BIG -> big-path list.
-__global__ void __launch_bounds__(1024) k_classify(Args a) {
+// The per-sub-bucket part of k_classify: starts and cursors, H1 for n' <= 1
+// (P:183), block windows, big-path items.
+__device__ __forceinline__ void classify_rest(const Args &a, uint64_t g, uint32_t st, uint32_t c, int sc, int lane) {
+    a.start1[g] = st;
+    a.cur1[g] = st;
+    if (sc == SC_TRIVIAL) {
+        if (a.dH1) a.dH1[g] = 1;
+    } else if (sc == SC_WINDOW) {  // tiny sub-buckets: block windows
+        // (the first / last window sub-bucket of each tile among this
+        // warp's lanes does the atomics: st and g grow with the lane)
+        const uint32_t t = st / a.T_tile;
+        const uint32_t wm = __activemask();
+        const uint32_t below = wm & ((1u << lane) - 1u), above = wm & ~((2u << lane) - 1u);
+        const uint32_t tp = __shfl_sync(wm, t, below ? 31 - __clz(below) : lane);
+        const uint32_t tn = __shfl_sync(wm, t, above ? __ffs(above) - 1 : lane);
+        if (!below || tp != t) atomicMin(&a.tile_first[t], (uint32_t)g);
+        if (!above || tn != t) atomicMax(&a.tile_last[t], (uint32_t)g);
+    } else if (sc == SC_BIG) {
+        const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
+        if (k < a.big_cap) {
+            uint32_t lrk = 0;  // large items: grid-parallel path (ls_bigpath.cu)
+            if (c > LARGE_MIN) {
+                const uint32_t li = atomicAdd(&a.ctl->nlarge, 1u);
+                if (li < a.lcap) {
+                    a.large[li] = k;
+                    lrk = li + 1u;
+                } else {
+                    atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+                }
+            }
+            a.big[k] = BigItem{st, c, 0u, (uint32_t)g, ~0ull, 0ull, lrk, 0u};
+            const uint32_t nch = (c + MM_CHUNK - 1) / MM_CHUNK;
+            const uint32_t base = atomicAdd(&a.ctl->nchunks, nch);
+            for (uint32_t q = 0; q < nch; q++)
+                if (base + q < a.chunk_cap) a.chunks[base + q] = BigChunk{k, q};
+                else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+        } else {
+            atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
+        }
+    }
+}
+
+// 256 threads x 4 sub-buckets per thread: the block is a chain of dependent
+// loads, barriers and one global atomic (latency-bound), so all f blocks are
+// made resident at once (8 per SM) instead of 2 per SM in waves.
+constexpr int CL_THREADS = 256;
+constexpr int CL_Q = LS_MAX_FANOUT / CL_THREADS;  // sub-buckets per thread
+static_assert(CL_Q * CL_THREADS == LS_MAX_FANOUT && CL_Q * (CL_THREADS / 32) == 32, "k_classify: 32 warp rows");
+__global__ void __launch_bounds__(CL_THREADS, 7) k_classify(Args a) {
     __shared__ uint32_t s[LS_MAX_FANOUT];
     __shared__ uint32_t tmp[33];
+    __shared__ uint32_t wcnt[5][32], wbase[5];
     const int b = blockIdx.x, f = a.f, tid = threadIdx.x;
+    const int lane = tid & 31, w = tid >> 5;
     const uint64_t row = (uint64_t)b * f;
     const uint64_t bbeg = a.start0[b], nb = a.start0[b + 1] - bbeg;
     const bool h0 = nb <= 1 || a.bmax0[b] == 0ull;
@@ -597,105 +647,80 @@ __global__ void __launch_bounds__(1024) k_classify(Args a) {
                 atomicAdd(&a.ctl->stat[ST_H0K], (unsigned long long)nb);
             }
         }
-        for (int j = tid; j < f; j += blockDim.x) {
+        for (int j = tid; j < f; j += CL_THREADS) {
             a.hist1[row + j] = 0;
             a.start1[row + j] = (uint32_t)bbeg;
         }
         return;
     }
-    for (int j = tid; j < f; j += blockDim.x) s[j] = a.hist1[row + j];
+    // sub-buckets q * CL_THREADS + tid, q < CL_Q: warp w's q-th group is the
+    // 32 consecutive sub-buckets of warp row q * 8 + w
+    uint32_t c[CL_Q];
+#pragma unroll
+    for (int q = 0; q < CL_Q; q++) {
+        const int j = q * CL_THREADS + tid;
+        c[q] = j < f ? a.hist1[row + j] : 0u;
+        if (j < f) s[j] = c[q];
+    }
     __syncthreads();
     const uint32_t total = block_exscan(s, f, tmp);
     if (tid == 0 && total != nb) atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-    // one sub-bucket per thread (f <= 1024 = blockDim.x)
-    const int j = tid;
-    const uint64_t g = row + (uint64_t)(j < f ? j : 0);
-    const uint32_t c = j < f ? a.hist1[g] : 0u;
-    const uint32_t st = j < f ? (uint32_t)bbeg + s[j] : 0u;
-    // SMALL sub-buckets of <= WS_MAX keys become warp tasks (compacted per
-    // block: one global atomic per level-0 bucket)
-    // (a bucket of the cluster-resident round 1 has its warp-sized
-    // sub-buckets sorted there already: k_round1's P5)
-    const int sc0 = j < f ? size_class(c, a.T_small) : SC_TRIVIAL;
-    const int sc = (sc0 == SC_WARP && a.fused[b]) ? SC_FUSED : sc0;
-    // warp / CTA sorts become task lists (compacted per block: one global
-    // atomic per level-0 bucket and class)
-    {
-        __shared__ uint32_t wcnt[5][32], wbase[5];
-        const int lane = tid & 31, w = tid >> 5;
-        uint32_t m[5];
-        m[0] = __ballot_sync(0xffffffffu, sc == SC_WARP);
-        m[1] = __ballot_sync(0xffffffffu, sc == SC_CTA);
-        m[2] = __ballot_sync(0xffffffffu, sc == SC_CTAM);
-        m[3] = __ballot_sync(0xffffffffu, sc == SC_CTAL);
-        m[4] = __ballot_sync(0xffffffffu, sc == SC_CTAS);
-        if (lane == 0)
-            for (int q = 0; q < 5; q++) wcnt[q][w] = __popc(m[q]);
-        __syncthreads();
-        if (tid < 5) {
-            uint32_t tot = 0;
-            for (int q = 0; q < (int)(blockDim.x >> 5); q++) {
-                const uint32_t t = wcnt[tid][q];
-                wcnt[tid][q] = tot;
-                tot += t;
-            }
-            uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask
-                          : tid == 2 ? &a.ctl->nctask2 : tid == 3 ? &a.ctl->nctask3 : &a.ctl->nctask4;
-            wbase[tid] = tot ? atomicAdd(ctr, tot) : 0u;
+    // SMALL sub-buckets of <= WS_MAX keys become warp tasks, larger ones CTA
+    // tasks (compacted per block: one global atomic per level-0 bucket and
+    // class). A bucket of the cluster-resident round 1 has its warp-sized
+    // sub-buckets sorted there already (k_round1's P5).
+    uint32_t st[CL_Q], m[CL_Q][5];
+    int sc[CL_Q];
+    const bool fused = a.fused[b];
+#pragma unroll
+    for (int q = 0; q < CL_Q; q++) {
+        const int j = q * CL_THREADS + tid;
+        st[q] = j < f ? (uint32_t)bbeg + s[j] : 0u;
+        const int sc0 = j < f ? size_class(c[q], a.T_small) : SC_TRIVIAL;
+        sc[q] = (sc0 == SC_WARP && fused) ? SC_FUSED : sc0;
+        m[q][0] = __ballot_sync(0xffffffffu, sc[q] == SC_WARP);
+        m[q][1] = __ballot_sync(0xffffffffu, sc[q] == SC_CTA);
+        m[q][2] = __ballot_sync(0xffffffffu, sc[q] == SC_CTAM);
+        m[q][3] = __ballot_sync(0xffffffffu, sc[q] == SC_CTAL);
+        m[q][4] = __ballot_sync(0xffffffffu, sc[q] == SC_CTAS);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 5; k++) wcnt[k][q * (CL_THREADS / 32) + w] = __popc(m[q][k]);
         }
-        __syncthreads();
-        const int c2 = sc == SC_WARP ? 0 : sc == SC_CTA ? 1 : sc == SC_CTAM ? 2 : sc == SC_CTAL ? 3 : sc == SC_CTAS ? 4 : -1;
-        // warp tasks carry the leaf that holds all their keys (+1; 0: none)
-        const uint32_t wl = (m[0] | m[1] | m[2] | m[3] | m[4])
-                                ? contained_leaf_warp(a.M->leaf, (int)a.M->L, (uint32_t)(row + (tid & ~31)),
+    }
+    __syncthreads();
+    if (tid < 5) {
+        uint32_t tot = 0;
+        for (int r = 0; r < 32; r++) {
+            const uint32_t t = wcnt[tid][r];
+            wcnt[tid][r] = tot;
+            tot += t;
+        }
+        uint32_t *ctr = tid == 0 ? &a.ctl->ntask : tid == 1 ? &a.ctl->nctask
+                      : tid == 2 ? &a.ctl->nctask2 : tid == 3 ? &a.ctl->nctask3 : &a.ctl->nctask4;
+        wbase[tid] = tot ? atomicAdd(ctr, tot) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < CL_Q; q++) {
+        const int j = q * CL_THREADS + tid;
+        const int wr = q * (CL_THREADS / 32) + w;
+        const uint64_t g = row + (uint64_t)(j < f ? j : 0);
+        const int c2 = sc[q] == SC_WARP ? 0 : sc[q] == SC_CTA ? 1 : sc[q] == SC_CTAM ? 2
+                     : sc[q] == SC_CTAL ? 3 : sc[q] == SC_CTAS ? 4 : -1;
+        // tasks carry the leaf that holds all their keys (+1; 0: none)
+        const uint32_t wl = (m[q][0] | m[q][1] | m[q][2] | m[q][3] | m[q][4])
+                                ? contained_leaf_warp(a.M->leaf, (int)a.M->L, (uint32_t)(row + (j & ~31)),
                                                       (uint32_t)g, a.rcpF2, lane)
                                 : 0u;
         if (c2 >= 0) {
-            const uint32_t k = wbase[c2] + wcnt[c2][w] + __popc(m[c2] & ((1u << lane) - 1u));
+            const uint32_t mc = c2 == 0 ? m[q][0] : c2 == 1 ? m[q][1] : c2 == 2 ? m[q][2] : c2 == 3 ? m[q][3] : m[q][4];
+            const uint32_t k = wbase[c2] + wcnt[c2][wr] + __popc(mc & ((1u << lane) - 1u));
             uint4 *list = c2 == 0 ? a.tasks : c2 == 1 ? a.ctasks : c2 == 2 ? a.ctasks2 : c2 == 3 ? a.ctasks3 : a.ctasks4;
-            if (k < a.task_cap) list[k] = make_uint4(st, c, (uint32_t)g, wl);
+            if (k < a.task_cap) list[k] = make_uint4(st[q], c[q], (uint32_t)g, wl);
             else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
         }
-    }
-    if (j < f) {
-        a.start1[g] = st;
-        a.cur1[g] = st;
-        if (sc == SC_TRIVIAL) {
-            if (a.dH1) a.dH1[g] = 1;
-        } else if (sc == SC_WINDOW) {  // tiny sub-buckets: block windows
-            // (the first / last window sub-bucket of each tile among this
-            // warp's lanes does the atomics: st and g grow with the lane)
-            const uint32_t t = st / a.T_tile;
-            const uint32_t wm = __activemask();
-            const int lane = tid & 31;
-            const uint32_t below = wm & ((1u << lane) - 1u), above = wm & ~((2u << lane) - 1u);
-            const uint32_t tp = __shfl_sync(wm, t, below ? 31 - __clz(below) : lane);
-            const uint32_t tn = __shfl_sync(wm, t, above ? __ffs(above) - 1 : lane);
-            if (!below || tp != t) atomicMin(&a.tile_first[t], (uint32_t)g);
-            if (!above || tn != t) atomicMax(&a.tile_last[t], (uint32_t)g);
-        } else if (sc == SC_BIG) {
-            const uint32_t k = atomicAdd(&a.ctl->big_cnt[0], 1u);
-            if (k < a.big_cap) {
-                uint32_t lrk = 0;  // large items: grid-parallel path (ls_bigpath.cu)
-                if (c > LARGE_MIN) {
-                    const uint32_t li = atomicAdd(&a.ctl->nlarge, 1u);
-                    if (li < a.lcap) {
-                        a.large[li] = k;
-                        lrk = li + 1u;
-                    } else {
-                        atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-                    }
-                }
-                a.big[k] = BigItem{st, c, 0u, (uint32_t)g, ~0ull, 0ull, lrk, 0u};
-                const uint32_t nch = (c + MM_CHUNK - 1) / MM_CHUNK;
-                const uint32_t base = atomicAdd(&a.ctl->nchunks, nch);
-                for (uint32_t q = 0; q < nch; q++)
-                    if (base + q < a.chunk_cap) a.chunks[base + q] = BigChunk{k, q};
-                    else atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-            } else {
-                atomicOr(&a.ctl->status, (uint32_t)STATUS_INTERNAL);
-            }
-        }
+        if (j < f) classify_rest(a, g, st[q], c[q], sc[q], lane);
     }
 }
 
@@ -793,7 +818,7 @@ void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
 }
 void launch_classify(const Args &a, uint32_t *dS_B1, cudaStream_t st) {
     (void)dS_B1;
-    k_classify<<<a.f, 1024, 0, st>>>(a);
+    k_classify<<<a.f, CL_THREADS, 0, st>>>(a);
 }
 void launch_bucket_ids(const uint64_t *keys, uint64_t n, int f, const DevModel *M, double *p,
                        uint32_t *b0, uint32_t *b1, unsigned long long *h0, unsigned long long *h1,
