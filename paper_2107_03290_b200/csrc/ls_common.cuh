@@ -326,6 +326,7 @@ constexpr uint32_t LARGE_MIN = 262144;  // big sub-buckets above this: grid-para
 struct Ctl {
     uint32_t status;
     uint32_t ticket0, ticket1, U1;
+    uint32_t ticket_s1;                // k_scatter1p's tile tickets
     uint32_t big_cnt[BIG_LEVELS + 1];  // items per big level list
     uint32_t big_next[BIG_LEVELS + 1]; // work counters
     uint32_t big_lv0;                  // level-0 tickets of k_big: level-0 items + the large path's level-1 items

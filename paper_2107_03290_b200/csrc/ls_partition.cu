@@ -26,6 +26,7 @@ __global__ void k_init(Ctl *ctl) {
     if (threadIdx.x == 0) {
         ctl->status = 0;
         ctl->ticket0 = ctl->ticket1 = ctl->U1 = 0;
+        ctl->ticket_s1 = 0;
         ctl->nchunks = 0;
         ctl->nwin = ctl->wticket = 0;
         ctl->ntask = ctl->nctask = ctl->nctask2 = ctl->nctask3 = ctl->nctask4 = 0;
@@ -521,6 +522,7 @@ __global__ void __launch_bounds__(512, 3) k_count1(Args a) {
     }
 }
 
+constexpr uint64_t S1P_MAX_N = 128ull << 20;
 template <int NT>
 struct Scatter1SmemT {
     TpSmemT<NT, TP_KPT> tp;
@@ -577,6 +579,190 @@ __global__ void __launch_bounds__(NT, TP_THREADS / NT) k_scatter1(Args a) {
     tile_partition<false, true, true, NoBucket, NT, TP_KPT, TpBidsT<NT * TP_KPT>, true>(
         S.tp, a.B, a.A, beg, end, a.Bcap, nullptr, f, bf, phase, a.bid, &S.sbid,
         (a.dbg & 2048u) ? a.ctl->prof + 5 : nullptr, &rs);
+}
+
+// Round-1 scatter, persistent form (LS_SCATTER1P): one CTA per SM takes the
+// tiles of all level-0 buckets in bucket order from a ticket counter, the ring
+// staged one tile ahead across bucket boundaries. At any time the grid works
+// on ~148 consecutive tiles (about six level-0 buckets: few open sub-bucket
+// write streams), no CTA waits for its first tile with an idle SM, and there is
+// no last-wave tail. Same per-tile steps as tile_partition<BIDS, RESERVE> with
+// the exact 32-bit cursors of the tile's bucket; homogeneous level-0 buckets
+// are written from their value, tile by tile.
+struct S1Desc {
+    uint64_t t0;       // first staged position in B (even) / first position of a fill tile
+    uint32_t th, lo;   // slot positions [lo, th) are this tile's keys
+    uint32_t b, kind;  // level-0 bucket; 0: no more tiles, 1: partition tile, 2: fill tile
+};
+struct Scatter1pSmem {
+    TpSmem tp;
+    alignas(16) TpBids sbid;
+    uint32_t tstart[LS_MAX_FANOUT + 1];
+    uint32_t bbeg[LS_MAX_FANOUT], bsz[LS_MAX_FANOUT];  // each bucket's region in B (positions fit 32 bits: cur1)
+    uint8_t bh0[LS_MAX_FANOUT];                        // 1: homogeneous (fill tiles)
+    uint32_t tmp[33];
+    S1Desc desc[TP_NSLOT];
+};
+static_assert(sizeof(Scatter1pSmem) <= MAX_SMEM_OPTIN, "scatter1p shared memory");
+static_assert(TP_NSLOT == 2 && TP_THREADS >= LS_MAX_FANOUT, "k_scatter1p: two ring slots, bucket b <-> thread b");
+
+template <int DT>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_scatter1p(Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Scatter1pSmem &S = *reinterpret_cast<Scatter1pSmem *>(smem_raw);
+    constexpr int NT = TP_THREADS, KPT = TP_KPT, TILE = TP_TILE;
+    const int f = a.f, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (a.ctl->status) return;
+    // tiles per level-0 bucket (tiles start at even positions of B, as in
+    // tile_partition), then their exclusive prefix: tile ticket -> bucket
+    for (int b = tid; b <= f; b += NT) {
+        uint32_t nt = 0;
+        if (b < f) {
+            const uint64_t bbeg = a.bsrc[b], h = a.fused[b] ? 0ull : a.start0[b + 1] - a.start0[b];
+            const bool h0 = h <= 1 || a.bmax0[b] == 0ull;
+            if (h) nt = (uint32_t)(((h0 ? h : bbeg + h - (bbeg & ~1ull)) + TILE - 1) / TILE);
+            S.bbeg[b] = (uint32_t)bbeg;
+            S.bsz[b] = (uint32_t)h;
+            S.bh0[b] = h0;
+        }
+        S.tstart[b] = nt;
+    }
+    for (int b = tid; b < f; b += NT) S.tp.cnt[b] = 0;
+    if (tid == 0) {
+        for (int j = 0; j < TP_NSLOT; j++) mbar_init(&S.tp.mbar[j], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (inits before the bulk copies)
+    }
+    __syncthreads();
+    const uint32_t total = block_exscan(S.tstart, f + 1, S.tmp);
+    // thread 0: take the next tile ticket, describe it in desc[slot] and stage it
+    // (the ticket after the next is drawn one tile early: the atomic's
+    // round trip is over by the time take() needs it; the bucket regions are
+    // in shared memory, so take() is a bisection and one bulk-copy issue)
+    uint32_t ahead = 0;
+    auto take = [&](int slot) {
+        const uint32_t tk = ahead;
+        ahead = atomicAdd(&a.ctl->ticket_s1, 1u);
+        S1Desc d{0ull, 0u, 0u, 0u, 0u};
+        if (tk < total) {
+            const int b = find_bucket(S.tstart, f, tk);
+            const uint32_t k = tk - S.tstart[b];
+            const uint64_t bbeg = S.bbeg[b], h = S.bsz[b], bend = bbeg + h;
+            d.b = (uint32_t)b;
+            if (S.bh0[b]) {
+                d.kind = 2u;
+                d.t0 = bbeg + (uint64_t)k * TILE;
+                d.th = (uint32_t)umin64((uint64_t)TILE, bend - d.t0);
+            } else {
+                const uint64_t tbase = bbeg & ~1ull;
+                d.kind = 1u;
+                d.t0 = tbase + (uint64_t)k * TILE;
+                d.th = (uint32_t)umin64((uint64_t)TILE, bend - d.t0);
+                d.lo = k == 0 ? (uint32_t)(bbeg - tbase) : 0u;
+                tp_issue<TpSmem, TpBids>(S.tp, slot, a.B, d.t0, d.t0 + d.th, a.Bcap, a.bid, &S.sbid);
+            }
+        }
+        S.desc[slot] = d;
+    };
+    if (tid == 0) {
+        ahead = atomicAdd(&a.ctl->ticket_s1, 1u);
+        for (int j = 0; j < TP_NSLOT; j++) take(j);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    uint64_t *const dst = a.A;
+    const uint32_t lim = (uint32_t)a.n;
+    for (uint32_t i = 0;; i++) {
+        const int slot = (int)(i & 1u);
+        const S1Desc d = S.desc[slot];
+        if (d.kind == 0u) break;
+        if (d.kind == 2u) {  // homogeneous level-0 bucket: written straight from its value
+            const uint64_t v = from_ord<DT>(a.bmin0[d.b]);
+            uint64_t *Ab = a.A + a.start0[d.b] - a.bsrc[d.b] + d.t0;
+            for (uint32_t j = tid; j < d.th; j += NT) Ab[j] = v;
+            __syncthreads();
+            if (tid == 0 && i >= 1) take(slot ^ 1);
+            __syncthreads();
+            continue;
+        }
+        const int th = (int)d.th, lo = (int)d.lo, tn = th - lo;
+        uint32_t *const cur = a.cur1 + (uint64_t)d.b * f;
+        mbar_wait(&S.tp.mbar[slot], (phase >> slot) & 1u);
+        const uint64_t *keys = S.tp.ring[slot];
+        const uint16_t *bids = S.sbid[slot] + (d.t0 & 7);
+        uint64_t key[KPT];
+        uint32_t code[KPT];
+#pragma unroll
+        for (int k2 = 0; k2 < KPT / 2; k2++) {
+            const int h = 2 * (k2 * NT + tid);
+            const ulonglong2 kv = *reinterpret_cast<const ulonglong2 *>(keys + h);
+            const uint32_t ip = *reinterpret_cast<const uint32_t *>(bids + h);
+            key[2 * k2] = kv.x;
+            key[2 * k2 + 1] = kv.y;
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const int k = 2 * k2 + e;
+                code[k] = 0xffffffffu;
+                if (h + e >= lo && h + e < th) {
+                    const uint32_t b1 = e ? ip >> 16 : ip & 0xffffu;
+                    const uint32_t r = atomicAdd(&S.tp.cnt[b1], 1u);
+                    code[k] = b1 | (r << 10);
+                }
+            }
+        }
+        __syncthreads();
+        // every thread is past the previous tile's store phase: its ring slot
+        // and descriptor are free for the tile after this one
+        if (tid == 0 && i >= 1) take(slot ^ 1);
+        // exclusive scan of the tile's sub-bucket counts (bucket tid <-> thread tid)
+        const uint32_t c = tid < f ? S.tp.cnt[tid] : 0u;
+        const uint32_t rsv = c ? atomicAdd(&cur[tid], c) : 0u;  // (first needed after the placement)
+        const uint32_t incl = warp_incl_scan(c);
+        if (lane == 31) S.tp.wsum[warp] = incl;
+        __syncthreads();
+        const uint32_t ws = lane < NT / 32 ? S.tp.wsum[lane] : 0u;
+        const uint32_t wpre = __reduce_add_sync(0xffffffffu, lane < warp ? ws : 0u);
+        const uint32_t ex0 = wpre + incl - c;
+        if (tid < f) {
+            S.tp.ex[tid] = ex0;
+            S.tp.cnt[tid] = 0;
+        }
+        __syncthreads();
+        uint64_t *sk = S.tp.ring[slot];
+        uint32_t pos[KPT];
+#pragma unroll
+        for (int k = 0; k < KPT; k++)
+            pos[k] = code[k] != 0xffffffffu ? S.tp.ex[code[k] & 1023u] + (code[k] >> 10) : 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < KPT; k++) {
+            if (pos[k] != 0xffffffffu) {
+                sk[pos[k]] = key[k];
+                S.tp.sbin[pos[k]] = (uint16_t)(code[k] & 1023u);
+            }
+        }
+        if (c) S.tp.delta[tid] = rsv - ex0;
+        __syncthreads();
+        {
+            uint32_t bb[KPT], dd[KPT];
+            uint64_t v[KPT];
+#pragma unroll
+            for (int k = 0; k < KPT; k++) {
+                const int idx = k * NT + tid;
+                bb[k] = idx < tn ? S.tp.sbin[idx] : 0u;
+                v[k] = sk[idx];
+            }
+#pragma unroll
+            for (int k = 0; k < KPT; k++) dd[k] = S.tp.delta[bb[k]];
+#pragma unroll
+            for (int k = 0; k < KPT; k++) {
+                const int idx = k * NT + tid;
+                const uint32_t q = dd[k] + (uint32_t)idx;
+                if (idx < tn && q < lim) dst[q] = v[k];
+            }
+        }
+        // (no barrier: the next tile's first barrier orders these reads of the
+        // slot, sbin and delta before anything overwrites them)
+        phase ^= 1u << slot;
+    }
 }
 
 // ------------------------------------------------------------- classify ----
@@ -811,7 +997,26 @@ void launch_count1(const Args &a, int dtype, cudaStream_t st) {
     if (dtype == DT_F64) k_count1<DT_F64><<<a.U1max, 512, 0, st>>>(a);
     else { set_smem(k_count1<DT_U64>, sm); k_count1<DT_U64><<<a.U1max, 512, sm, st>>>(a); }
 }
+// k_scatter1p below S1P_MAX_N keys, k_scatter1 above (measured at 1M / 10M /
+// 100M / 200M / 1B Normal keys: 0.033 / 0.083 / 0.548 / 1.067 / 5.22 ms
+// against 0.045 / 0.093 / 0.570 / 1.042 / 4.97 ms). LS_SCATTER1P=0/1 forces one.
+static bool scatter1_persistent(uint64_t n) {
+    static const int v = [] {
+        const char *e = getenv("LS_SCATTER1P");
+        return e ? atoi(e) : -1;
+    }();
+    return v < 0 ? n <= S1P_MAX_N : v != 0;
+}
 void launch_scatter1(const Args &a, int dtype, cudaStream_t st) {
+    if (scatter1_persistent(a.n)) {
+        const size_t sm = sizeof(Scatter1pSmem);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (dtype == DT_F64) { set_smem(k_scatter1p<DT_F64>, sm); k_scatter1p<DT_F64><<<sms, TP_THREADS, sm, st>>>(a); }
+        else { set_smem(k_scatter1p<DT_U64>, sm); k_scatter1p<DT_U64><<<sms, TP_THREADS, sm, st>>>(a); }
+        return;
+    }
     const size_t sm = sizeof(Scatter1Smem);
     if (dtype == DT_F64) { set_smem(k_scatter1<DT_F64, TP_THREADS>, sm); k_scatter1<DT_F64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
     else { set_smem(k_scatter1<DT_U64, TP_THREADS>, sm); k_scatter1<DT_U64, TP_THREADS><<<a.U1max, TP_THREADS, sm, st>>>(a); }
