@@ -311,10 +311,39 @@ struct Timer {
         cudaEventRecord(ev[0], st);
         k = 0;
     }
+    // Under capture the event-record nodes sit on a branch of their own
+    // (`tst`): node k waits for the main sequence up to its mark and for node
+    // k-1, and nothing on the main sequence waits for it, so the kernels run
+    // back to back as they do without phase timing (in line, the 9 nodes cost
+    // ~0.06 ms per 200M-key sort). join() ties the branch back before the
+    // capture ends.
+    cudaStream_t tst = nullptr;
+    void rec_external(int i) {
+        cudaEvent_t d = nullptr;
+        if (tst && cudaEventCreateWithFlags(&d, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventRecord(d, st) == cudaSuccess && cudaStreamWaitEvent(tst, d, 0) == cudaSuccess) {
+            cudaEventRecordWithFlags(ev[i], tst, cudaEventRecordExternal);
+            branched = true;
+        } else {
+            cudaGetLastError();
+            cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal);
+        }
+        if (d) cudaEventDestroy(d);
+    }
+    bool branched = false;
+    void join() {
+        cudaEvent_t d = nullptr;
+        if (!on || !branched) return;
+        if (cudaEventCreateWithFlags(&d, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventRecord(d, tst);
+            cudaStreamWaitEvent(st, d, 0);
+            cudaEventDestroy(d);
+        }
+    }
     void mark(int phase) {
         if (!on) return;
         phase_of[k] = phase;
-        if (external) cudaEventRecordWithFlags(ev[++k], st, cudaEventRecordExternal);
+        if (external) rec_external(++k);
         else cudaEventRecord(ev[++k], st);
     }
     void finish(ls_stats *s) {
@@ -336,15 +365,15 @@ struct Timer {
 constexpr int LS_NSIDE = 5;
 static cudaStream_t side_stream(int k = 0) {
     constexpr int MAXD = 64;
-    static cudaStream_t s[MAXD][LS_NSIDE];
+    static cudaStream_t s[MAXD][LS_NSIDE + 1];  // (+ the phase-timing branch of a captured sequence)
     static std::once_flag once[MAXD];
     int d = -1;
-    if (k < 0 || k >= LS_NSIDE || cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXD) {
+    if (k < 0 || k > LS_NSIDE || cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXD) {
         cudaGetLastError();
         return nullptr;
     }
     std::call_once(once[d], [d] {
-        for (int j = 0; j < LS_NSIDE; j++)
+        for (int j = 0; j <= LS_NSIDE; j++)
             if (cudaStreamCreateWithFlags(&s[d][j], cudaStreamNonBlocking) != cudaSuccess) {
                 s[d][j] = nullptr;
                 cudaGetLastError();
@@ -622,9 +651,11 @@ static bool launch_graph(Args &a, const Layout &l, const ls_config &cfg, int dt,
             drop_events();
             return false;
         }
-        if (cap.on) cudaEventRecordWithFlags(cap.ev[0], cs[key.dev], cudaEventRecordExternal);
+        cap.tst = side_stream(LS_NSIDE);  // (the timing branch; nullptr: event nodes in line)
+        if (cap.on) cap.rec_external(0);
         uint64_t nl = 0;
         const ls_status r = launch_sequence(a, l, cfg, nullptr, nullptr, dt, key.ws, cap, cs[key.dev], nl);
+        cap.join();
         cudaGraph_t g = nullptr;
         const cudaError_t ec = cudaStreamEndCapture(cs[key.dev], &g);
         cudaGraphExec_t x = nullptr;
