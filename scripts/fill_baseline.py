@@ -8,15 +8,15 @@ import sys
 ROWS = [  # (config, label, workload, dtype, parity at full size / at 1e6-1e7)
     ("1", "Uniform[0,1)", "c1_uniform01", "fp64", "1e6/1e7 element-wise"),
     ("2", "Normal(0,1)", "c2_normal", "fp64", "200M element-wise + S_B/S'_B/H0/H1"),
-    ("2", "LogNormal(0,0.5)", "c2_lognormal", "fp64", "1e6/1e7 element-wise"),
-    ("2", "Exponential(λ=2)", "c2_exponential", "fp64", "1e6 element-wise"),
-    ("2", "5-Gaussian mix", "c2_mixgauss", "fp64", "1e6 element-wise"),
+    ("2", "LogNormal(0,0.5)", "c2_lognormal", "fp64", "200M element-wise + S_B/S'_B/H0/H1"),
+    ("2", "Exponential(λ=2)", "c2_exponential", "fp64", "200M element-wise + S_B/S'_B/H0/H1"),
+    ("2", "5-Gaussian mix", "c2_mixgauss", "fp64", "200M element-wise + S_B/S'_B/H0/H1"),
     ("3", "Zipf(0.75), 1M values", "c3_zipf", "u64", "200M element-wise + S_B/S'_B/H0/H1"),
-    ("3", "RootDups", "c3_rootdups", "u64", "1e6/1e7 element-wise"),
+    ("3", "RootDups", "c3_rootdups", "u64", "200M element-wise + S_B/S'_B/H0/H1"),
     ("3", "TwoDups", "c3_twodups", "u64", "200M element-wise + S_B/S'_B/H0/H1"),
     ("4", "telemetry levels + ID clusters", "c4_telemetry", "u64", "200M element-wise + S_B/S'_B/H0/H1"),
-    ("ref", "Uniform[0,1)", "ref_uniform01", "fp64", "1e6/1e7 element-wise"),
-    ("ref", "uniform u64", "ref_uniform_u64", "u64", "1e6 element-wise"),
+    ("ref", "Uniform[0,1)", "ref_uniform01", "fp64", "200M element-wise + S_B/S'_B/H0/H1"),
+    ("ref", "uniform u64", "ref_uniform_u64", "u64", "200M element-wise + S_B/S'_B/H0/H1"),
 ]
 
 

@@ -336,9 +336,11 @@ def test_determinism():
 # --------------------------------------------------------- full size (200M) -
 
 @pytest.mark.slow
-@pytest.mark.parametrize("dist", ["normal", "zipf", "telemetry", "twodups"])
+@pytest.mark.parametrize("dist", ["normal", "zipf", "telemetry", "twodups", "lognormal", "exponential",
+                                  "mixgauss", "rootdups", "uniform01", "uniform_u64"])
 def test_full_size_200m(dist):
-    """BASELINE configs 2-4 at full size, in the bench launch configuration
+    """BASELINE configs 2-4 and both reference rows (every 200M line bench.py
+    reports) at full size, in the bench launch configuration
     (same workspace, same default config, CUDA Graph replay on the second
     call): the sorted output equals the oracle's (Alg. 2 run on the same 200M
     bytes) element by element, and so do S_B, S'_B, H0, H1 and the
